@@ -1,0 +1,555 @@
+// collect-reduce / histogram on the GPU (aggregate.py:122-299), level by
+// level like the semisort scheduler.
+//
+// Per level: sample heavy keys; count the matrix while folding heavy values
+// into SMEM accumulators (heavy records never move, aggregate.py:156-157);
+// scan the light columns; scatter light records only into a compacted child
+// buffer (aggregate.py:159-165); light buckets >= alpha become next-level
+// nodes, smaller ones are folded in a shared-memory hash table (the
+// chained-hash group order of _base_fold, aggregate.py:239-264).  Integer
+// sums are order independent (wrapping uint64, aggregate.py:67-79), so the
+// result pairs are bit-exact.  Pairs are emitted in a deterministic order:
+// by level, heavy pairs by node then leaves by (node, bucket).
+#pragma once
+
+#include "engine.cuh"
+#include "leaf.cuh"
+#include "multisplit.cuh"
+#include "sample.cuh"
+#include "scan.cuh"
+#include "sort_engine.cuh"
+
+namespace ss {
+
+template <typename V> __device__ __forceinline__ uint64_t val_u64(const V& v) { return static_cast<uint64_t>(v); }
+template <> __device__ __forceinline__ uint64_t val_u64<NoVal>(const NoVal&) { return 0; }
+template <> __device__ __forceinline__ uint64_t val_u64<V16>(const V16& v) { return v.lo; }
+
+// Counting matrix + per-row heavy partial sums.
+template <typename K, typename V, bool SUM>
+__global__ void __launch_bounds__(kCountThreads)
+k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, const Work* __restrict__ work, uint32_t n_work,
+            const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, KeyBuckets bf,
+            unsigned long long* __restrict__ HS, uint32_t hs_stride) {
+  extern __shared__ __align__(16) uint32_t cnt[];
+  __shared__ HeavySmem tab;
+  __shared__ unsigned long long hsum[kMaxHeavyDevice];
+  for (uint32_t wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
+    const Work wk = work[wi];
+    const Node nd = nodes[wk.node];
+    bf.prepare(nd, wk.node, &tab);
+    const uint32_t nb = bf.n_buckets();
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+    if (SUM)
+      for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x) hsum[t] = 0;
+    __syncthreads();
+    const uint64_t begin = wk.begin;
+    const uint32_t len = wk.len;
+    const uint32_t nl = bf.n_light;
+    for (uint32_t base = 0; base < len; base += kCountThreads * kCountItems) {
+      K keys[kCountItems];
+#pragma unroll
+      for (int k = 0; k < kCountItems; ++k) {
+        uint32_t i = base + k * kCountThreads + threadIdx.x;
+        keys[k] = i < len ? ldg_key(src, begin + i) : K(0);
+      }
+#pragma unroll
+      for (int k = 0; k < kCountItems; ++k) {
+        uint32_t i = base + k * kCountThreads + threadIdx.x;
+        bool valid = i < len;
+        uint32_t act = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          uint32_t b = bf(keys[k], begin + i);
+          uint32_t peers = __match_any_sync(act, b);
+          const bool leader = lane_id() == __ffs(peers) - 1;
+          if (leader) atomicAdd(&cnt[b], __popc(peers));
+          if (SUM && b >= nl) {
+            uint64_t v = val_u64(sv[begin + i]);
+            uint64_t s = 0;
+            for (uint32_t m = peers; m; m &= m - 1) s += __shfl_sync(peers, v, __ffs(m) - 1);
+            if (leader) atomicAdd(&hsum[b - nl], static_cast<unsigned long long>(s));
+          }
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t* row = C + wk.row * stride;
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) row[b] = cnt[b];
+    if (SUM)
+      for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x) HS[wk.row * hs_stride + t] = hsum[t];
+    __syncthreads();
+  }
+}
+
+// Heavy totals per node: column sums of C (count) or of HS (sum64).
+template <typename K, bool SUM>
+__global__ void k_heavy_fold(const Node* __restrict__ nodes, uint32_t n_nodes, const uint32_t* __restrict__ C,
+                             uint32_t stride, uint32_t n_light, const unsigned long long* __restrict__ HS,
+                             uint32_t hs_stride, const uint64_t* __restrict__ heavy, uint32_t mh,
+                             K* __restrict__ hk, uint64_t* __restrict__ ha) {
+  for (uint32_t j = blockIdx.x; j < n_nodes; j += gridDim.x) {
+    const Node nd = nodes[j];
+    for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x) {
+      uint64_t s = 0;
+      for (uint32_t r = 0; r < nd.n_rows; ++r) {
+        const uint64_t row = nd.row_base + r;
+        s += SUM ? static_cast<uint64_t>(HS[row * hs_stride + t]) : C[row * stride + n_light + t];
+      }
+      hk[static_cast<uint64_t>(j) * mh + t] = static_cast<K>(heavy[static_cast<uint64_t>(j) * mh + t]);
+      ha[static_cast<uint64_t>(j) * mh + t] = s;
+    }
+  }
+}
+
+// Base fold of one leaf: groups in chained-hash order with count or sum.
+template <typename K, typename V, bool SUM>
+__device__ void leaf_fold(const K* rk, const V* rv, uint32_t m, bool identity, LeafArrays a, uint32_t* red,
+                          K* out_k, uint64_t* out_a, uint32_t* g_out) {
+  const uint32_t cap = leaf_cap(m);
+  leaf_group(rk, m, cap, identity, a);
+  if (SUM) {
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) a.gsum[s] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+      atomicAdd(&a.gsum[a.rslot[i]], static_cast<unsigned long long>(val_u64(rv[i])));
+  }
+  for (uint32_t c = threadIdx.x; c < cap; c += blockDim.x) a.cell[c] = 0;
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x)
+    if (a.T[s] != kEmpty32) atomicAdd(&a.cell[a.home[s]], 1u);
+  __syncthreads();
+  leaf_scan_cells(a.cell, cap, red);
+  leaf_group_starts(cap, a, true);
+  uint32_t groups = 0;
+  for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+    if (a.T[s] == kEmpty32) continue;
+    const uint32_t g = a.gstart[s];
+    out_k[g] = rk[a.T[s]];
+    out_a[g] = SUM ? static_cast<uint64_t>(a.gsum[s]) : a.gcnt[s];
+    ++groups;
+  }
+  uint32_t tot;
+  block_excl_scan<uint32_t>(groups, red, tot);
+  if (threadIdx.x == 0) *g_out = tot;
+}
+
+__host__ inline size_t leaf_fold_smem_bytes(int key_bytes, int val_bytes) {
+  return static_cast<size_t>(kLeafSmemMax) * (key_bytes + val_bytes) +
+         leaf_words(kLeafSmemMax, true) * 4 + 64;
+}
+
+template <typename K, typename V, bool SUM>
+__global__ void __launch_bounds__(kLeafThreads)
+k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, const Leaf* __restrict__ leaves,
+                 uint32_t n_leaves, int identity, K* __restrict__ st_k, uint64_t* __restrict__ st_a,
+                 uint32_t* __restrict__ G) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t red[33];
+  K* rk = reinterpret_cast<K*>(smem);
+  V* rv = reinterpret_cast<V*>(rk + kLeafSmemMax);
+  uint32_t* work = reinterpret_cast<uint32_t*>(SUM ? reinterpret_cast<unsigned char*>(rv + kLeafSmemMax)
+                                                   : reinterpret_cast<unsigned char*>(rv));
+  // gsum (u64) leads the work arrays: keep it 8-byte aligned
+  work = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(work) + 15) & ~uintptr_t(15));
+  for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
+    const Leaf lf = leaves[l];
+    const uint32_t m = static_cast<uint32_t>(lf.size);
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      rk[i] = src_k[lf.lo + i];
+      if (SUM) rv[i] = src_v[lf.lo + i];
+    }
+    __syncthreads();
+    const uint32_t cap = leaf_cap(m);
+    LeafArrays a = leaf_arrays(work, cap, m, true);
+    leaf_fold<K, V, SUM>(rk, rv, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l);
+    __syncthreads();
+  }
+}
+
+template <typename K, typename V, bool SUM>
+__global__ void __launch_bounds__(kLeafThreads)
+k_leaf_fold_global(const K* __restrict__ src_k, const V* __restrict__ src_v, const Leaf* __restrict__ leaves,
+                   uint32_t n_leaves, int identity, K* __restrict__ st_k, uint64_t* __restrict__ st_a,
+                   uint32_t* __restrict__ G, uint32_t* __restrict__ scratch, uint64_t words_per_cta) {
+  __shared__ uint32_t red[33];
+  uint32_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * words_per_cta;
+  for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
+    const Leaf lf = leaves[l];
+    const uint32_t m = static_cast<uint32_t>(lf.size);
+    LeafArrays a = leaf_arrays(mine, leaf_cap(m), m, true);
+    leaf_fold<K, V, SUM>(src_k + lf.lo, src_v + lf.lo, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l);
+    __syncthreads();
+  }
+}
+
+template <typename K>
+__global__ void k_emit_heavy(const Node* __restrict__ nodes, uint32_t n_nodes, const uint64_t* __restrict__ hoff,
+                             const K* __restrict__ hk, const uint64_t* __restrict__ ha, uint32_t mh,
+                             K* __restrict__ out_k, uint64_t* __restrict__ out_a, const uint64_t* __restrict__ cursor) {
+  const uint64_t c0 = *cursor;
+  for (uint32_t j = blockIdx.x; j < n_nodes; j += gridDim.x) {
+    const uint64_t base = c0 + hoff[j];
+    for (uint32_t t = threadIdx.x; t < nodes[j].n_heavy; t += blockDim.x) {
+      out_k[base + t] = hk[static_cast<uint64_t>(j) * mh + t];
+      out_a[base + t] = ha[static_cast<uint64_t>(j) * mh + t];
+    }
+  }
+}
+
+template <typename K>
+__global__ void k_emit_leaves(const Leaf* __restrict__ leaves, uint32_t n_leaves, const uint32_t* __restrict__ G,
+                              const uint64_t* __restrict__ loff, const K* __restrict__ st_k,
+                              const uint64_t* __restrict__ st_a, K* __restrict__ out_k, uint64_t* __restrict__ out_a,
+                              const uint64_t* __restrict__ cursor) {
+  const uint64_t c0 = *cursor;
+  // one warp per leaf
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < n_leaves; l += warps) {
+    const uint64_t base = c0 + loff[l], lo = leaves[l].lo;
+    const uint32_t g = G[l];
+    for (uint32_t t = lane_id(); t < g; t += 32) {
+      out_k[base + t] = st_k[lo + t];
+      out_a[base + t] = st_a[lo + t];
+    }
+  }
+}
+
+static __global__ void k_bump(uint64_t* cursor, const uint64_t* add_dev, uint64_t add_host) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cursor += (add_dev ? *add_dev : 0) + add_host;
+}
+
+template <typename K, typename V>
+struct AggEngine {
+  static constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  const K* in_k = nullptr;
+  const V* in_v = nullptr;
+  uint64_t n = 0;
+  int kind = SS_AGG_COUNT;
+  int identity = 0;
+  Params P{};
+  cudaStream_t st = nullptr;
+  ss_telemetry* tel = nullptr;
+
+  uint32_t stride = 0, mh = 1, sample_grid = 0, leafg_grid = 0;
+  uint64_t max_nodes = 0, max_rows = 0, max_grps = 0, max_leaves = 0, s_cap = 0, leafg_words = 0, max_pairs = 0;
+  // workspace; d_out_* first so ss_result_copy can find them with a minimal carve
+  K* d_out_k = nullptr;
+  uint64_t* d_out_a = nullptr;
+  K* B_k[2] = {nullptr, nullptr};
+  V* B_v[2] = {nullptr, nullptr};
+  K* st_k = nullptr;
+  uint64_t* st_a = nullptr;
+  Node* d_nodes = nullptr;
+  Node* d_next = nullptr;
+  uint64_t* d_heavy = nullptr;
+  Work* d_work = nullptr;
+  uint32_t* d_grp_node = nullptr;
+  uint32_t* d_C = nullptr;
+  uint64_t* d_X = nullptr;
+  uint64_t* d_P = nullptr;
+  uint64_t* d_off = nullptr;
+  uint32_t* d_ccnt = nullptr;
+  uint64_t* d_misc = nullptr;
+  Leaf* d_leaf_s = nullptr;
+  Leaf* d_leaf_g = nullptr;
+  uint64_t* d_samp = nullptr;
+  uint32_t* d_leafscr = nullptr;
+  unsigned long long* d_HS = nullptr;
+  uint64_t* d_ntot = nullptr;
+  uint64_t* d_nbase = nullptr;
+  uint32_t* d_G = nullptr;
+  uint64_t* d_loff = nullptr;
+  uint64_t* d_part = nullptr;
+  K* d_hk = nullptr;
+  uint64_t* d_ha = nullptr;
+  uint64_t* d_hoff = nullptr;
+  uint64_t* d_cursor = nullptr;
+
+  void plan(Arena& a) {
+    stride = even_stride(P);
+    mh = std::max<uint32_t>(P.max_heavy, 1);
+    const uint64_t alpha = P.base_case_cutoff;
+    max_nodes = std::max<uint64_t>(1, n / alpha);
+    max_rows = kTargetRows + max_nodes;
+    max_grps = max_rows / kRowGroup + max_nodes + 1;
+    max_leaves = std::max<uint64_t>(1, std::min<uint64_t>(n, max_nodes * P.light_buckets));
+    s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
+    sample_grid = static_cast<uint32_t>(std::min<uint64_t>(kSampleGridMax, max_nodes));
+    const uint64_t mmax = std::max<uint64_t>(1, std::min<uint64_t>(n, alpha > 1 ? alpha - 1 : 1));
+    leafg_words = leaf_words(mmax, true);
+    leafg_grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kLeafGlobalGridMax, cdiv(n, kLeafSmemMax + 1))));
+    max_pairs = std::max<uint64_t>(n, 1);
+    d_out_k = a.take<K>(max_pairs);
+    d_out_a = a.take<uint64_t>(max_pairs);
+    d_cursor = a.take<uint64_t>(1);
+    for (int i = 0; i < 2; ++i) {
+      B_k[i] = a.take<K>(n);
+      if (kHasV) B_v[i] = a.take<V>(n);
+    }
+    st_k = a.take<K>(n);
+    st_a = a.take<uint64_t>(n);
+    d_nodes = a.take<Node>(max_nodes);
+    d_next = a.take<Node>(max_nodes);
+    d_heavy = a.take<uint64_t>(max_nodes * mh);
+    d_work = a.take<Work>(max_rows);
+    d_grp_node = a.take<uint32_t>(max_grps);
+    d_C = a.take<uint32_t>(max_rows * stride);
+    d_X = a.take<uint64_t>(max_rows * stride);
+    d_P = a.take<uint64_t>(max_grps * stride);
+    d_off = a.take<uint64_t>(max_nodes * (stride + 1));
+    d_ccnt = a.take<uint32_t>(max_nodes * 3);
+    d_misc = a.take<uint64_t>(8);
+    d_leaf_s = a.take<Leaf>(max_leaves);
+    d_leaf_g = a.take<Leaf>(max_leaves);
+    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * (2 * s_cap + 2 * pow2_ge(s_cap)));
+    d_leafscr = a.take<uint32_t>(static_cast<uint64_t>(leafg_grid) * leafg_words);
+    d_HS = a.take<unsigned long long>(max_rows * mh);
+    d_ntot = a.take<uint64_t>(max_nodes);
+    d_nbase = a.take<uint64_t>(max_nodes);
+    d_G = a.take<uint32_t>(max_leaves);
+    d_loff = a.take<uint64_t>(max_leaves);
+    d_part = a.take<uint64_t>(scan_parts_needed(std::max(max_leaves, max_nodes)) + 8);
+    d_hk = a.take<K>(max_nodes * mh);
+    d_ha = a.take<uint64_t>(max_nodes * mh);
+    d_hoff = a.take<uint64_t>(max_nodes);
+  }
+
+  bool sum() const { return kind == SS_AGG_SUM64; }
+
+  // fold + emit one device leaf list living in `src`
+  void fold_list(Tracker& tr, const K* sk, const V* sv, const Leaf* d_list, uint64_t count, bool smem_ok,
+                 uint32_t* scr, uint64_t words, uint32_t grid_cap) {
+    if (!count) return;
+    const uint32_t cnt = static_cast<uint32_t>(count);
+    if (smem_ok) {
+      const size_t sm = leaf_fold_smem_bytes(sizeof(K), sum() ? ValTraits<V>::bytes : 0);
+      const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148 * 2));
+      if (sum()) {
+        auto kern = k_leaf_fold_smem<K, V, true>;
+        SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G);
+      } else {
+        auto kern = k_leaf_fold_smem<K, V, false>;
+        SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G);
+      }
+      if (tel) tel->leaves_smem += count;
+    } else {
+      const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, grid_cap));
+      if (sum())
+        k_leaf_fold_global<K, V, true><<<grid, kLeafThreads, 0, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G,
+                                                                     scr, words);
+      else
+        k_leaf_fold_global<K, V, false><<<grid, kLeafThreads, 0, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G,
+                                                                      scr, words);
+      if (tel) tel->leaves_global += count;
+    }
+    check_launch();
+    device_exclusive_scan<uint32_t>(d_G, count, d_loff, d_part, d_misc + 6, st);
+    k_emit_leaves<K><<<static_cast<uint32_t>(std::min<uint64_t>(cdiv(count, 8), 148 * 16)), 256, 0, st>>>(
+        d_list, cnt, d_G, d_loff, st_k, st_a, d_out_k, d_out_a, d_cursor);
+    k_bump<<<1, 32, 0, st>>>(d_cursor, d_misc + 6, 0);
+    check_launch();
+    tr.launched(6);
+  }
+
+  // host-built leaves of any size (root leaf, forced leaves)
+  void fold_host(Tracker& tr, const K* sk, const V* sv, const std::vector<Leaf>& leaves) {
+    const uint64_t mmax = std::max<uint64_t>(1, std::min<uint64_t>(n, P.base_case_cutoff > 1 ? P.base_case_cutoff - 1 : 1));
+    for (const Leaf& l : leaves) {
+      SS_CUDA(cudaMemcpyAsync(d_leaf_g, &l, sizeof(Leaf), cudaMemcpyHostToDevice, st));
+      if (l.size <= kLeafSmemMax) {
+        fold_list(tr, sk, sv, d_leaf_g, 1, true, nullptr, 0, 1);
+      } else if (l.size <= mmax) {
+        fold_list(tr, sk, sv, d_leaf_g, 1, false, d_leafscr, leafg_words, 1);
+      } else {
+        const uint64_t words = leaf_words(l.size, true);
+        uint32_t* scr = nullptr;
+        SS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scr), words * 4, st));
+        fold_list(tr, sk, sv, d_leaf_g, 1, false, scr, words, 1);
+        SS_CUDA(cudaFreeAsync(scr, st));
+      }
+      SS_CUDA(cudaStreamSynchronize(st));   // &l must outlive the copy
+    }
+  }
+
+  std::vector<Node> level(Tracker& tr, std::vector<Node>& cur, int lvl) {
+    const K* sk = lvl == 1 ? in_k : B_k[lvl & 1];
+    const V* sv = lvl == 1 ? in_v : B_v[lvl & 1];
+    K* dk = B_k[(lvl + 1) & 1];
+    V* dv = B_v[(lvl + 1) & 1];
+    const uint32_t nn = static_cast<uint32_t>(cur.size());
+    uint64_t R = 0;
+    for (auto& nd : cur) R += nd.size;
+    const uint64_t chunk = std::max<uint64_t>(kMinChunk, cdiv(R, kTargetRows));
+    std::vector<Work> work;
+    std::vector<uint32_t> grp_node;
+    for (uint32_t j = 0; j < nn; ++j) {
+      Node& nd = cur[j];
+      nd.row_base = work.size();
+      nd.n_rows = static_cast<uint32_t>(cdiv(nd.size, chunk));
+      nd.grp_base = static_cast<uint32_t>(grp_node.size());
+      nd.n_grps = static_cast<uint32_t>(cdiv(nd.n_rows, kRowGroup));
+      for (uint32_t r = 0; r < nd.n_rows; ++r) {
+        Work w;
+        w.begin = nd.lo + r * chunk;
+        w.len = static_cast<uint32_t>(std::min<uint64_t>(chunk, nd.size - r * chunk));
+        w.node = j;
+        w.row = nd.row_base + r;
+        work.push_back(w);
+      }
+      for (uint32_t g = 0; g < nd.n_grps; ++g) grp_node.push_back(j);
+    }
+    if (work.size() > max_rows || grp_node.size() > max_grps || nn > max_nodes)
+      throw Fail(SS_ERR_RESOURCE, "level plan exceeds workspace bounds");
+    const uint32_t nwork = static_cast<uint32_t>(work.size());
+    const uint32_t ngrp = static_cast<uint32_t>(grp_node.size());
+    SS_CUDA(cudaMemcpyAsync(d_nodes, cur.data(), nn * sizeof(Node), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemcpyAsync(d_work, work.data(), nwork * sizeof(Work), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemcpyAsync(d_grp_node, grp_node.data(), ngrp * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+
+    tr.begin(kPhSample);
+    SS_CUDA(cudaFuncSetAttribute(k_sample<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSampleSmem)));
+    k_sample<K><<<std::min<uint32_t>(sample_grid, nn), kSampleThreads, kSampleSmem, st>>>(
+        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0);
+    check_launch();
+    tr.launched();
+
+    KeyBuckets bf{};
+    bf.heavy = d_heavy;
+    bf.max_heavy = mh;
+    bf.n_light = P.light_buckets;
+    bf.light_bits = P.light_bits;
+    bf.identity = identity;
+
+    tr.begin(kPhCount);
+    if (sum())
+      k_count_agg<K, V, true><<<nwork, kCountThreads, stride * 4, st>>>(sk, sv, d_work, nwork, d_nodes, d_C, stride, bf,
+                                                                        d_HS, mh);
+    else
+      k_count_agg<K, V, false><<<nwork, kCountThreads, stride * 4, st>>>(sk, sv, d_work, nwork, d_nodes, d_C, stride,
+                                                                         bf, d_HS, mh);
+    check_launch();
+    tr.launched();
+
+    tr.begin(kPhScan);
+    k_colsum_groups<uint32_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, stride, P.light_buckets, 1, 0);
+    k_scan_nodes<<<nn, 1024, 0, st>>>(d_nodes, nn, d_P, d_off, stride, P.light_buckets, 1, 0, d_ntot);
+    device_exclusive_scan<uint64_t>(d_ntot, nn, d_nbase, d_part, d_misc + 5, st);
+    k_write_X<uint32_t, uint64_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, d_X, stride,
+                                                         P.light_buckets, 1, 0, d_nbase);
+    check_launch();
+    tr.launched(6);
+
+    tr.begin(kPhDistribute);
+    const size_t dsm = dist_smem_bytes(stride, sizeof(K), ValTraits<V>::bytes);
+    auto dkern = k_distribute<K, V, KeyBuckets>;
+    SS_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
+    dkern<<<nwork, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets, bf);
+    check_launch();
+    tr.launched();
+
+    tr.begin(kPhCopy);
+    if (sum())
+      k_heavy_fold<K, true><<<nn, 128, 0, st>>>(d_nodes, nn, d_C, stride, P.light_buckets, d_HS, mh, d_heavy, mh, d_hk, d_ha);
+    else
+      k_heavy_fold<K, false><<<nn, 128, 0, st>>>(d_nodes, nn, d_C, stride, P.light_buckets, d_HS, mh, d_heavy, mh, d_hk,
+                                                 d_ha);
+    check_launch();
+    tr.launched();
+
+    tr.begin(kPhChildren);
+    SS_CUDA(cudaMemsetAsync(d_misc, 0, 5 * sizeof(uint64_t), st));
+    k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff, kLeafSmemMax,
+                                         d_ccnt);
+    k_children_scan<<<1, 1024, 0, st>>>(d_ccnt, nn, d_misc);
+    k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff, kLeafSmemMax,
+                                        d_ccnt, d_nbase, rounds_per_hash(P.light_bits), d_leaf_s, d_leaf_g, d_next,
+                                        d_misc + 3);
+    check_launch();
+    tr.launched(3);
+    tr.end();
+
+    uint64_t misc[8];
+    std::vector<uint64_t> ntot(nn);
+    SS_CUDA(cudaMemcpyAsync(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaMemcpyAsync(cur.data(), d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaMemcpyAsync(ntot.data(), d_ntot, nn * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    const uint64_t n_s = misc[0], n_g = misc[1], n_next = misc[2];
+    std::vector<Node> next(n_next);
+    if (n_next) {
+      SS_CUDA(cudaMemcpyAsync(next.data(), d_next, n_next * sizeof(Node), cudaMemcpyDeviceToHost, st));
+      SS_CUDA(cudaStreamSynchronize(st));
+    }
+    if (tel) {
+      for (uint32_t j = 0; j < nn; ++j) {
+        tel->bucket_assignments += cur[j].size;
+        if (lvl <= 64)
+          tel->matrix_cells_by_level[lvl] += cdiv(cur[j].size, P.subarray_len) * (P.light_buckets + cur[j].n_heavy);
+        tel->scratch_moves += ntot[j];
+      }
+      const uint64_t kids = n_s + n_g + n_next;
+      tel->nodes += kids;
+      if (kids && static_cast<uint64_t>(lvl + 1) > tel->max_depth) tel->max_depth = lvl + 1;
+      tel->levels += 1;
+    }
+
+    // emit: heavy pairs (by node), then leaves (by node, bucket)
+    tr.begin(kPhLeaves);
+    std::vector<uint64_t> hoff(nn);
+    uint64_t htot = 0;
+    for (uint32_t j = 0; j < nn; ++j) {
+      hoff[j] = htot;
+      htot += cur[j].n_heavy;
+    }
+    if (htot) {
+      SS_CUDA(cudaMemcpyAsync(d_hoff, hoff.data(), nn * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+      k_emit_heavy<K><<<std::min<uint32_t>(nn, 1184), 128, 0, st>>>(d_nodes, nn, d_hoff, d_hk, d_ha, mh, d_out_k, d_out_a,
+                                                                   d_cursor);
+      k_bump<<<1, 32, 0, st>>>(d_cursor, nullptr, htot);
+      check_launch();
+      tr.launched(2);
+    }
+    fold_list(tr, dk, dv, d_leaf_s, n_s, true, nullptr, 0, 1);
+    fold_list(tr, dk, dv, d_leaf_g, n_g, false, d_leafscr, leafg_words, leafg_grid);
+    std::vector<Node> keep;
+    std::vector<Leaf> forced;
+    for (const Node& c : next) {
+      if (c.stalled >= 2 || lvl + 1 >= kDepthLimit) forced.push_back(Leaf{c.lo, c.size});
+      else keep.push_back(c);
+    }
+    fold_host(tr, dk, dv, forced);
+    SS_CUDA(cudaStreamSynchronize(st));   // hoff must outlive its copy
+    tr.end();
+    return keep;
+  }
+
+  uint64_t run(Tracker& tr) {
+    SS_CUDA(cudaMemsetAsync(d_cursor, 0, sizeof(uint64_t), st));
+    if (tel) {
+      tel->nodes += 1;
+      tel->max_depth = std::max<uint64_t>(tel->max_depth, 1);
+    }
+    if (n == 0) return 0;
+    if (n < P.base_case_cutoff) {
+      fold_host(tr, in_k, in_v, {Leaf{0, n}});
+    } else {
+      Node root{};
+      root.lo = 0;
+      root.size = n;
+      std::vector<Node> cur{root};
+      int lvl = 1;
+      while (!cur.empty()) {
+        cur = level(tr, cur, lvl);
+        ++lvl;
+      }
+    }
+    uint64_t count = 0;
+    SS_CUDA(cudaMemcpyAsync(&count, d_cursor, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    return count;
+  }
+};
+
+}  // namespace ss

@@ -1,0 +1,219 @@
+// Shared device primitives for the B200 semisort hot path (sm_100a).
+//
+// Everything here is integer work: the splitmix64 finalizer the reference
+// uses as its key hash (hashing.py:25-47), the numpy-compatible
+// Philox4x64-10 stream that drives sampling (core.py:238-239, numpy's
+// Generator.integers -> Lemire bounded draws), the per-depth light-id bit
+// slice (core.py:139-151), and a shared-memory heavy-key table
+// (core.py:64-104, 193-213).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ss {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;   // hashing.py:14
+constexpr uint64_t kMul1 = 0xBF58476D1CE4E5B9ull;    // hashing.py:15
+constexpr uint64_t kMul2 = 0x94D049BB133111EBull;    // hashing.py:16
+constexpr int kDepthLimit = 64;                      // core.py:39
+constexpr uint32_t kNoBucket = 0xFFFFFFFFu;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  uint64_t z = x + kGamma;
+  z = (z ^ (z >> 30)) * kMul1;
+  z = (z ^ (z >> 27)) * kMul2;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64_pair(uint64_t a, uint64_t b) {
+  return mix64(a ^ mix64(b));
+}
+
+// Value payload of a record: the reference's values column may be absent or
+// any fixed-width layout; the hot path only moves it.
+struct NoVal {};
+struct alignas(16) V16 { uint64_t lo, hi; };
+
+template <typename T> struct ValTraits { static constexpr int bytes = sizeof(T); };
+template <> struct ValTraits<NoVal> { static constexpr int bytes = 0; };
+
+template <typename V>
+__device__ __forceinline__ V load_val(const V* p, uint64_t i) { return p[i]; }
+template <>
+__device__ __forceinline__ NoVal load_val<NoVal>(const NoVal*, uint64_t) { return NoVal{}; }
+template <typename V>
+__device__ __forceinline__ void store_val(V* p, uint64_t i, const V& v) { p[i] = v; }
+template <>
+__device__ __forceinline__ void store_val<NoVal>(NoVal*, uint64_t, const NoVal&) {}
+
+// Read-only streaming load of one key.
+template <typename K>
+__device__ __forceinline__ K ldg_key(const K* p, uint64_t i) { return __ldg(p + i); }
+
+// ---------------------------------------------------------------------------
+// key hash and light ids
+// ---------------------------------------------------------------------------
+
+template <typename K>
+__device__ __forceinline__ uint64_t key_hash(K key, bool identity) {
+  uint64_t k = static_cast<uint64_t>(key);   // u32 keys widen (adapters.py:113)
+  return identity ? k : mix64(k);
+}
+
+// Per-node light-id slice: rnd, slot = divmod(depth, rounds) (core.py:146-151).
+struct LightCfg {
+  uint64_t salt;     // mix64(rnd), used when remix != 0
+  uint32_t shift;    // slot * light_bits
+  uint32_t mask;     // n_light - 1
+  uint32_t remix;    // rnd > 0
+
+  __host__ __device__ static LightCfg make(uint32_t depth, uint32_t light_bits, uint32_t n_light) {
+    uint32_t rounds = 64u / (light_bits > 1 ? light_bits : 1u);
+    if (rounds < 1) rounds = 1;
+    uint32_t rnd = depth / rounds, slot = depth % rounds;
+    LightCfg c;
+    c.salt = mix64(static_cast<uint64_t>(rnd));
+    c.shift = slot * light_bits;
+    c.mask = n_light - 1;
+    c.remix = rnd != 0;
+    return c;
+  }
+  __device__ __forceinline__ uint32_t id(uint64_t h) const {
+    if (remix) h = mix64(h ^ salt);
+    return static_cast<uint32_t>(h >> shift) & mask;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// shared-memory heavy table: key -> heavy slot (discovery order)
+// ---------------------------------------------------------------------------
+
+constexpr int kHeavySlots = 1024;   // >= 2 * max_heavy (500); power of two
+constexpr int kMaxHeavyDevice = 512;
+
+struct HeavySmem {
+  uint64_t keys[kHeavySlots];
+  unsigned short ids[kHeavySlots];
+};
+
+__device__ __forceinline__ uint32_t heavy_home(uint64_t key) {
+  return static_cast<uint32_t>((key * kGamma) >> 54) & (kHeavySlots - 1);
+}
+
+// Cooperative parallel build; caller must __syncthreads() afterwards.
+__device__ __forceinline__ void heavy_build(HeavySmem& t, const uint64_t* heavy, uint32_t n_heavy) {
+  for (int s = threadIdx.x; s < kHeavySlots; s += blockDim.x) t.ids[s] = 0xFFFF;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_heavy; i += blockDim.x) {
+    uint64_t k = heavy[i];
+    uint32_t s = heavy_home(k);
+    while (atomicCAS(&t.ids[s], static_cast<unsigned short>(0xFFFF), static_cast<unsigned short>(i)) != 0xFFFF)
+      s = (s + 1) & (kHeavySlots - 1);
+    t.keys[s] = k;
+  }
+}
+
+// Returns the heavy slot of key or -1.
+__device__ __forceinline__ int heavy_find(const HeavySmem& t, uint64_t key) {
+  uint32_t s = heavy_home(key);
+  while (true) {
+    uint16_t id = t.ids[s];
+    if (id == 0xFFFF) return -1;
+    if (t.keys[s] == key) return id;
+    s = (s + 1) & (kHeavySlots - 1);
+  }
+}
+
+// Bucket id of a key at a node: heavy -> n_light + slot, else the light slice.
+template <typename K>
+__device__ __forceinline__ uint32_t bucket_of(K key, const HeavySmem& t, uint32_t n_heavy,
+                                              const LightCfg& lc, bool identity, uint32_t n_light) {
+  uint64_t k = static_cast<uint64_t>(key);
+  if (n_heavy) {
+    int h = heavy_find(t, k);
+    if (h >= 0) return n_light + static_cast<uint32_t>(h);
+  }
+  return lc.id(identity ? k : mix64(k));
+}
+
+// ---------------------------------------------------------------------------
+// numpy Philox4x64-10 + Generator.integers(0, m) (Lemire, no masking)
+// ---------------------------------------------------------------------------
+
+struct U64x4 { uint64_t v[4]; };
+
+__host__ __device__ __forceinline__ void mulhilo64(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
+#ifdef __CUDA_ARCH__
+  lo = a * b;
+  hi = __umul64hi(a, b);
+#else
+  unsigned __int128 p = static_cast<unsigned __int128>(a) * b;
+  lo = static_cast<uint64_t>(p);
+  hi = static_cast<uint64_t>(p >> 64);
+#endif
+}
+
+// Counter block `ctr` (numpy increments the 256-bit counter before each
+// block, so block j of a fresh generator uses counter j+1), key (k0, 0).
+__host__ __device__ __forceinline__ U64x4 philox4x64_10(uint64_t ctr, uint64_t k0) {
+  uint64_t c0 = ctr, c1 = 0, c2 = 0, c3 = 0, k1 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B97F4A7C15ull; k1 += 0xBB67AE8584CAA73Bull; }
+    uint64_t hi0, lo0, hi1, lo1;
+    mulhilo64(0xD2E7470EE14C6C93ull, c0, hi0, lo0);
+    mulhilo64(0xCA5A826395121157ull, c2, hi1, lo1);
+    uint64_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  U64x4 out;
+  out.v[0] = c0; out.v[1] = c1; out.v[2] = c2; out.v[3] = c3;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane_id() >= d) v += o;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; `tmp` needs
+// blockDim/32 + 1 entries.  Returns the exclusive prefix, writes the total.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* tmp, T& total) {
+  T inc = warp_incl_scan(v);
+  const int w = warp_id(), nw = blockDim.x >> 5;
+  if (lane_id() == 31) tmp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T x = lane_id() < nw ? tmp[lane_id()] : T(0);
+    T xi = warp_incl_scan(x);
+    if (lane_id() < nw) tmp[lane_id()] = xi - x;
+    if (lane_id() == nw - 1) tmp[32] = xi;
+  }
+  __syncthreads();
+  T out = tmp[w] + inc - v;
+  total = tmp[32];
+  __syncthreads();
+  return out;
+}
+
+}  // namespace ss

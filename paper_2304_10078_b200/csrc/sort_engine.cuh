@@ -1,0 +1,352 @@
+// Level-synchronous semisort scheduler (core.py:437-598 re-designed for the
+// GPU).
+//
+// The reference recurses node by node (big buckets sequentially,
+// core.py:496-498).  Every node's result depends only on its own descriptor
+// (range, depth, path, stall state), so we process all nodes of a recursion
+// level together: one launch per phase for the whole level, with one
+// device->host sync per level to learn the next level's node list.  Leaves
+// (light buckets < alpha) are resolved right after the level that produced
+// them.  Buffer roles follow core.py:117-131 / PAPER §3.4: level L reads A
+// when L is odd and S when L is even; heavy buckets written to S are copied
+// back, leaves living in S are written to A by their base case.
+#pragma once
+
+#include "engine.cuh"
+#include "leaf.cuh"
+#include "multisplit.cuh"
+#include "sample.cuh"
+
+namespace ss {
+
+constexpr uint64_t kTargetRows = 148 * 8;    // subarrays per level (~8 per SM)
+constexpr uint64_t kMinChunk = 4096;
+constexpr uint32_t kSampleGridMax = 148;
+constexpr uint32_t kLeafSmemGrid = 148 * 3;
+constexpr uint32_t kLeafGlobalGridMax = 296;
+constexpr size_t kSampleSmem = kSampleSmemCap * 4;
+
+inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
+  return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
+}
+
+template <typename K, typename V>
+struct SortEngine {
+  static constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  // inputs
+  K* A_k;
+  V* A_v;
+  uint64_t n;
+  int mode;
+  int identity;
+  Params P;
+  cudaStream_t st;
+  ss_telemetry* tel;
+  // plan
+  uint32_t stride = 0;
+  uint64_t max_nodes = 0, max_rows = 0, max_grps = 0, max_leaves = 0, s_cap = 0, leafg_words = 0;
+  uint32_t sample_grid = 0, leafg_grid = 0;
+  // workspace
+  K* S_k = nullptr;
+  V* S_v = nullptr;
+  Node* d_nodes = nullptr;
+  Node* d_next = nullptr;
+  uint64_t* d_heavy = nullptr;
+  Work* d_work = nullptr;
+  uint32_t* d_grp_node = nullptr;
+  uint32_t* d_C = nullptr;
+  uint64_t* d_X = nullptr;
+  uint64_t* d_P = nullptr;
+  uint64_t* d_off = nullptr;
+  uint32_t* d_ccnt = nullptr;
+  uint64_t* d_misc = nullptr;
+  Leaf* d_leaf_s = nullptr;
+  Leaf* d_leaf_g = nullptr;
+  uint64_t* d_samp = nullptr;
+  uint32_t* d_leafscr = nullptr;
+  bool external_scratch = false;
+
+  void plan(Arena& a, bool carve_scratch = true) {
+    stride = even_stride(P);
+    const uint64_t alpha = P.base_case_cutoff;
+    max_nodes = std::max<uint64_t>(1, n / alpha);
+    max_rows = kTargetRows + max_nodes;
+    max_grps = max_rows / kRowGroup + max_nodes + 1;
+    max_leaves = std::max<uint64_t>(1, std::min<uint64_t>(n, max_nodes * P.light_buckets));
+    s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
+    sample_grid = static_cast<uint32_t>(std::min<uint64_t>(kSampleGridMax, max_nodes));
+    const uint64_t mmax = std::max<uint64_t>(1, std::min<uint64_t>(n, alpha > 1 ? alpha - 1 : 1));
+    leafg_words = std::max(leaf_words(mmax, false), lt_leaf_words(mmax, sizeof(K)));
+    leafg_grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kLeafGlobalGridMax, cdiv(n, kLeafSmemMax + 1))));
+    if (carve_scratch) {
+      S_k = a.take<K>(n);
+      if (kHasV) S_v = a.take<V>(n);
+    }
+    d_nodes = a.take<Node>(max_nodes);
+    d_next = a.take<Node>(max_nodes);
+    d_heavy = a.take<uint64_t>(max_nodes * std::max<uint32_t>(P.max_heavy, 1));
+    d_work = a.take<Work>(max_rows);
+    d_grp_node = a.take<uint32_t>(max_grps);
+    d_C = a.take<uint32_t>(max_rows * stride);
+    d_X = a.take<uint64_t>(max_rows * stride);
+    d_P = a.take<uint64_t>(max_grps * stride);
+    d_off = a.take<uint64_t>(max_nodes * (stride + 1));
+    d_ccnt = a.take<uint32_t>(max_nodes * 3);
+    d_misc = a.take<uint64_t>(8);
+    d_leaf_s = a.take<Leaf>(max_leaves);
+    d_leaf_g = a.take<Leaf>(max_leaves);
+    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * (2 * s_cap + 2 * pow2_ge(s_cap)));
+    d_leafscr = a.take<uint32_t>(static_cast<uint64_t>(leafg_grid) * leafg_words);
+  }
+
+  bool src_is_A(int level, bool flip) const { return ((level & 1) == 1) != flip; }
+
+  // ---- leaves ---------------------------------------------------------------
+  void run_leaves_smem(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a) {
+    if (!count) return;
+    if (mode == SS_MODE_LT) {
+      run_leaves_global(tr, d_list, count, in_a, nullptr, 0);
+      return;
+    }
+    const size_t smem = leaf_smem_bytes(sizeof(K), kHasV ? sizeof(V) : 0);
+    auto kern = k_leaf_eq_smem<K, V>;
+    SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, kLeafSmemGrid));
+    kern<<<grid, kLeafThreads, smem, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v, d_list,
+                                           static_cast<uint32_t>(count), identity);
+    check_launch();
+    tr.launched();
+    if (tel) tel->leaves_smem += count;
+  }
+
+  // Global-scratch leaves; scr == nullptr uses the planned scratch.
+  void run_leaves_global(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a, uint32_t* scr,
+                         uint64_t words) {
+    if (!count) return;
+    uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, leafg_grid));
+    if (!scr) { scr = d_leafscr; words = leafg_words; }
+    else grid = 1;
+    if (mode == SS_MODE_LT) {
+      k_leaf_lt<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count),
+                                                    in_a, scr, words);
+    } else {
+      k_leaf_eq_global<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list,
+                                                            static_cast<uint32_t>(count), in_a, identity, scr, words);
+    }
+    check_launch();
+    tr.launched();
+    if (tel) tel->leaves_global += count;
+  }
+
+  // Leaves built on the host (root leaf, local_refine small buckets, forced
+  // leaves after a stall / at DEPTH_LIMIT): any size.
+  void run_host_leaves(Tracker& tr, const std::vector<Leaf>& leaves, bool in_a) {
+    if (leaves.empty()) return;
+    std::vector<Leaf> small, mid, huge;
+    const uint64_t mmax_planned = std::max<uint64_t>(1, std::min<uint64_t>(n, P.base_case_cutoff > 1 ? P.base_case_cutoff - 1 : 1));
+    for (const Leaf& l : leaves) {
+      if (l.size <= kLeafSmemMax && mode == SS_MODE_EQ) small.push_back(l);
+      else if (l.size <= mmax_planned) mid.push_back(l);
+      else huge.push_back(l);
+    }
+    if (!small.empty()) {
+      SS_CUDA(cudaMemcpyAsync(d_leaf_s, small.data(), small.size() * sizeof(Leaf), cudaMemcpyHostToDevice, st));
+      run_leaves_smem(tr, d_leaf_s, small.size(), in_a);
+    }
+    if (!mid.empty()) {
+      SS_CUDA(cudaMemcpyAsync(d_leaf_g, mid.data(), mid.size() * sizeof(Leaf), cudaMemcpyHostToDevice, st));
+      run_leaves_global(tr, d_leaf_g, mid.size(), in_a, nullptr, 0);
+    }
+    for (const Leaf& l : huge) {
+      // rare: a stalled bucket larger than alpha; dedicated scratch
+      const uint64_t words = std::max(leaf_words(l.size, false), lt_leaf_words(l.size, sizeof(K)));
+      uint32_t* scr = nullptr;
+      SS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scr), words * 4, st));
+      SS_CUDA(cudaMemcpyAsync(d_leaf_g, &l, sizeof(Leaf), cudaMemcpyHostToDevice, st));
+      run_leaves_global(tr, d_leaf_g, 1, in_a, scr, words);
+      SS_CUDA(cudaFreeAsync(scr, st));
+    }
+    // the host vectors must outlive the async copies
+    SS_CUDA(cudaStreamSynchronize(st));
+  }
+
+  // ---- one recursion level -------------------------------------------------
+  std::vector<Node> level(Tracker& tr, std::vector<Node>& cur, int lvl, bool flip) {
+    const bool from_a = src_is_A(lvl, flip);
+    const K* sk = from_a ? A_k : S_k;
+    const V* sv = from_a ? A_v : S_v;
+    K* dk = from_a ? S_k : A_k;
+    V* dv = from_a ? S_v : A_v;
+    const uint32_t nn = static_cast<uint32_t>(cur.size());
+
+    uint64_t R = 0;
+    for (auto& nd : cur) R += nd.size;
+    const uint64_t chunk = std::max<uint64_t>(kMinChunk, cdiv(R, kTargetRows));
+    std::vector<Work> work;
+    std::vector<uint32_t> grp_node;
+    for (uint32_t j = 0; j < nn; ++j) {
+      Node& nd = cur[j];
+      nd.out_base = nd.lo;
+      nd.row_base = work.size();
+      nd.n_rows = static_cast<uint32_t>(cdiv(nd.size, chunk));
+      nd.grp_base = static_cast<uint32_t>(grp_node.size());
+      nd.n_grps = static_cast<uint32_t>(cdiv(nd.n_rows, kRowGroup));
+      for (uint32_t r = 0; r < nd.n_rows; ++r) {
+        Work w;
+        w.begin = nd.lo + r * chunk;
+        w.len = static_cast<uint32_t>(std::min<uint64_t>(chunk, nd.size - r * chunk));
+        w.node = j;
+        w.row = nd.row_base + r;
+        work.push_back(w);
+      }
+      for (uint32_t g = 0; g < nd.n_grps; ++g) grp_node.push_back(j);
+    }
+    if (work.size() > max_rows || grp_node.size() > max_grps || nn > max_nodes)
+      throw Fail(SS_ERR_RESOURCE, "level plan exceeds workspace bounds");
+    const uint32_t nwork = static_cast<uint32_t>(work.size());
+    const uint32_t ngrp = static_cast<uint32_t>(grp_node.size());
+    tr.begin(kPhOther);
+    SS_CUDA(cudaMemcpyAsync(d_nodes, cur.data(), nn * sizeof(Node), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemcpyAsync(d_work, work.data(), nwork * sizeof(Work), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemcpyAsync(d_grp_node, grp_node.data(), ngrp * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+
+    // sampling + heavy tables
+    tr.begin(kPhSample);
+    SS_CUDA(cudaFuncSetAttribute(k_sample<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSampleSmem)));
+    k_sample<K><<<std::min<uint32_t>(sample_grid, nn), kSampleThreads, kSampleSmem, st>>>(
+        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0);
+    check_launch();
+    tr.launched();
+
+    KeyBuckets bf{};
+    bf.heavy = d_heavy;
+    bf.max_heavy = std::max<uint32_t>(P.max_heavy, 1);
+    bf.n_light = P.light_buckets;
+    bf.light_bits = P.light_bits;
+    bf.identity = identity;
+
+    // counting matrix
+    tr.begin(kPhCount);
+    k_count<K, KeyBuckets><<<nwork, kCountThreads, stride * 4, st>>>(sk, d_work, nwork, d_nodes, d_C, stride, bf);
+    check_launch();
+    tr.launched();
+
+    // column-major scan -> X, offsets
+    tr.begin(kPhScan);
+    k_colsum_groups<uint32_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, stride, P.light_buckets, 0, 0);
+    check_launch();
+    k_scan_nodes<<<nn, 1024, 0, st>>>(d_nodes, nn, d_P, d_off, stride, P.light_buckets, 0, 0, nullptr);
+    check_launch();
+    k_write_X<uint32_t, uint64_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, d_X, stride,
+                                               P.light_buckets, 0, 0, nullptr);
+    check_launch();
+    tr.launched(3);
+
+    // blocked distributing
+    tr.begin(kPhDistribute);
+    const size_t dsm = dist_smem_bytes(stride, sizeof(K), kHasV ? sizeof(V) : 0);
+    auto dkern = k_distribute<K, V, KeyBuckets>;
+    SS_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
+    dkern<<<nwork, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu, bf);
+    check_launch();
+    tr.launched();
+
+    // heavy buckets are final: copy them back when they landed in S
+    if (from_a) {
+      tr.begin(kPhCopy);
+      const uint32_t gy = std::min<uint32_t>(nn, 65535);
+      const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(1184, gy))));
+      k_copy_heavy<K, V><<<dim3(gx, gy), 256, 0, st>>>(S_k, S_v, A_k, A_v, d_nodes, nn, d_off, stride,
+                                                      P.light_buckets);
+      check_launch();
+      tr.launched();
+    }
+
+    // children
+    tr.begin(kPhChildren);
+    SS_CUDA(cudaMemsetAsync(d_misc, 0, 8 * sizeof(uint64_t), st));
+    k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff,
+                                         kLeafSmemMax, d_ccnt);
+    check_launch();
+    k_children_scan<<<1, 1024, 0, st>>>(d_ccnt, nn, d_misc);
+    check_launch();
+    k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff,
+                                        kLeafSmemMax, d_ccnt, nullptr, rounds_per_hash(P.light_bits),
+                                        d_leaf_s, d_leaf_g, d_next, d_misc + 3);
+    check_launch();
+    tr.launched(3);
+    tr.end();
+
+    uint64_t misc[8];
+    SS_CUDA(cudaMemcpyAsync(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaMemcpyAsync(cur.data(), d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    const uint64_t n_s = misc[0], n_g = misc[1], n_next = misc[2];
+    std::vector<Node> next(n_next);
+    if (n_next) {
+      SS_CUDA(cudaMemcpyAsync(next.data(), d_next, n_next * sizeof(Node), cudaMemcpyDeviceToHost, st));
+      SS_CUDA(cudaStreamSynchronize(st));
+    }
+
+    // telemetry with the reference's counter semantics (core.py:451-482)
+    if (tel) {
+      for (const Node& nd : cur) {
+        tel->bucket_assignments += nd.size;
+        if (lvl <= 64)
+          tel->matrix_cells_by_level[lvl] += cdiv(nd.size, P.subarray_len) * (P.light_buckets + nd.n_heavy);
+        if (from_a) tel->scratch_moves += nd.size;
+      }
+      const uint64_t kids = n_s + n_g + n_next;
+      tel->nodes += kids;
+      if (kids && static_cast<uint64_t>(lvl + 1) > tel->max_depth) tel->max_depth = lvl + 1;
+      tel->levels += 1;
+    }
+
+    // leaves of this level live on the destination side
+    const bool leaves_in_a = !from_a;
+    tr.begin(kPhLeaves);
+    run_leaves_smem(tr, d_leaf_s, n_s, leaves_in_a);
+    run_leaves_global(tr, d_leaf_g, n_g, leaves_in_a, nullptr, 0);
+
+    // forced leaves (stall valve / depth limit, core.py:459)
+    std::vector<Node> keep;
+    std::vector<Leaf> forced;
+    for (const Node& c : next) {
+      if (c.stalled >= 2 || lvl + 1 >= kDepthLimit) forced.push_back(Leaf{c.lo, c.size});
+      else keep.push_back(c);
+    }
+    run_host_leaves(tr, forced, leaves_in_a);
+    tr.end();
+    return keep;
+  }
+
+  // Drive levels from an initial frontier of internal nodes at `lvl`.
+  void drive(Tracker& tr, std::vector<Node> cur, int lvl, bool flip) {
+    while (!cur.empty()) {
+      cur = level(tr, cur, lvl, flip);
+      ++lvl;
+    }
+  }
+
+  void run(Tracker& tr) {
+    if (tel) tel->scratch_allocations += 1;   // one scratch per call (core.py:591-592)
+    if (tel) {
+      tel->nodes += 1;
+      tel->max_depth = std::max<uint64_t>(tel->max_depth, 1);
+    }
+    if (n == 0) return;
+    if (n < P.base_case_cutoff) {   // root is a leaf (core.py:459)
+      run_host_leaves(tr, {Leaf{0, n}}, true);
+      return;
+    }
+    Node root{};
+    root.lo = 0;
+    root.size = n;
+    root.path = 0;
+    root.depth = 0;
+    root.stalled = 0;
+    drive(tr, {root}, 1, false);
+  }
+};
+
+}  // namespace ss
