@@ -1,0 +1,334 @@
+"""Benchmark: semisort Grecords/s on BASELINE.json's headline config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the metric's config): semisort of
+n = 10^9 (uint64 key, uint64 value) records per GPU; keys Zipf(s=1.2) ranks
+over [1, 10^9] hashed to 64 bits (key = mix64(rank - 1)), value = global
+record index.  Synthetic, seeded, generated on the device (same family,
+parameters and sampler as the reference generator).
+N > 1: weak scaling, 10^9 records per rank, hash-partition + NCCL
+all_to_all_v + local semisort (paper_2304_10078_b200.distributed).
+
+Timing: W untimed warm-up steps, then K steps; before every step the input
+is restored from a pristine device copy (16 GB write: flushes the 126 MB
+L2), then barrier + synchronize, CUDA events around the library call only
+(the reference protocol, cli.py:94-109), max over ranks.  `e2e` repeats the
+step through the public API from pinned host buffers with the H2D input
+copy and the D2H result copy inside the timed region.  `cpu_baseline` times
+the CPU oracle (the reference algorithm restated in numpy) on a bounded
+sample of the same workload on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 10**9
+ZIPF_S = 1.2
+UNIVERSE = 10**9
+B_ALG = 72          # K + 4R bytes / record (semisort, 8 B keys, 16 B records)
+NOMINAL_HBM = 8.0e12
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline(n_sample: int, repeats: int = 1):
+    """The oracle (reference algorithm, numpy) on a bounded sample."""
+    import numpy as np
+
+    import oracle as O
+    from oracle.datagen import gen_keys_values
+    ranks, _ = gen_keys_values("zipfian", ZIPF_S, n_sample, 64, seed=1)
+    keys = O.mix64_np(ranks - np.uint64(1))
+    vals = np.arange(n_sample, dtype=np.uint64)
+    P = O.OracleParams.derive(n_sample)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.semisort(keys, vals, P)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return {"value": n_sample / t / 1e9, "unit": "Grecords/s", "cores": 1, "kind": "port",
+            "sample": f"semisort of {n_sample} records, Zipf s=1.2 ranks over [1, n_sample] hashed, "
+                      f"value=index; reference algorithm restated in numpy (oracle/), single thread; "
+                      f"best of {repeats}, {t:.2f} s"}
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle port on a bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as O
+    from oracle.datagen import gen_keys_values
+    n = args.ref_n
+    ranks, _ = gen_keys_values("zipfian", ZIPF_S, n, 64, seed=1)
+    keys = O.mix64_np(ranks - np.uint64(1))
+    vals = np.arange(n, dtype=np.uint64)
+    P = O.OracleParams.derive(n)
+    for _ in range(args.warmup):
+        O.semisort(keys, vals, P)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.semisort(keys, vals, P)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = n / dt / 1e9
+    line = {"metric": "semisort Grecords/s (n=1e9 u64 k/v, Zipf 1.2 hashed)", "value": v, "unit": "Grecords/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"c2 semisort sample n={n} (bounded CPU sample of the 1e9 workload)",
+                       "key": "Zipf(1.2) rank over [1, n] -> mix64(rank-1)", "value": "index"},
+            "cpu_baseline": {"value": v, "unit": "Grecords/s", "cores": 1, "kind": "port",
+                             "sample": f"{n} records per step, numpy restatement of the reference algorithm "
+                                       "(oracle/), single thread (the reference's worker pool does not "
+                                       "speed this path up, SURVEY.md Appendix A)"},
+            "e2e": {"value": v, "unit": "Grecords/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="records per GPU")
+    ap.add_argument("--e2e-n", type=int, default=None, help="records for the e2e leg (default n)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=1 << 22)
+    ap.add_argument("--ref-n", type=int, default=1 << 22)
+    ap.add_argument("--validate", action="store_true", help="check the last output (O(n) device checks)")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2304_10078_b200 as S
+    from paper_2304_10078_b200.datagen import generate_device
+    from paper_2304_10078_b200.distributed import dist_semisort
+
+    n = args.n
+    src = generate_device("zipfian", ZIPF_S, n, key_bits=64, seed=1, universe=UNIVERSE, hash_ranks=True,
+                          values="index", first_index=rank * n, device=dev)
+    work = src.copy()
+    adp = S.UIntKeyAdapter()
+    params = S.TuningParams.for_input(n)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    tel_last = S.Telemetry(timing=True)
+
+    def one_step(timed_tel=None):
+        work.keys.copy_(src.keys)
+        work.values.copy_(src.values)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        if world == 1:
+            S.semisort(work, adp, "eq", params, telemetry=timed_tel)
+            out = work
+        else:
+            out = dist_semisort(work, adp, telemetry=timed_tel)
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1), out
+
+    for _ in range(args.warmup):
+        one_step()
+    times, launches = [], 0
+    tel = S.Telemetry(timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t, out = one_step(tel)
+            times.append(t)
+    launches = tel.kernel_launches
+    ms = sum(times) / len(times)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    total_records = n * world
+    value = total_records / (ms / 1e3) / 1e9
+    peak_gbs, peak_kind = measured_peaks()
+
+    # dominant kernel: the blocked-distributing scatter (all levels of a step)
+    steps = args.steps
+    dist_ms = tel.phase_ms.get("distribute", 0.0) / steps
+    moved = 0
+    # records scattered per step = bucket assignments (each bucketed record is
+    # read once and written once by the distribute kernel)
+    moved = tel.bucket_assignments / steps
+    key_b, rec_b = 8, 16
+    achieved = (moved * 2 * rec_b) / (dist_ms / 1e3) / 1e9 if dist_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("k_distribute_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_achieved = B_ALG * n / (ms / 1e3) / 1e9   # per GPU, GB/s against the 72 B/rec model
+
+    valid = None
+    if args.validate and world == 1:
+        from paper_2304_10078_b200.validate import count_distinct, validate_indexed
+        rep = validate_indexed(src.keys, work.keys, work.values, count_distinct(src.keys))
+        valid = bool(rep.valid)
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        en = args.e2e_n or n
+        hk = torch.empty(en, dtype=torch.uint64, pin_memory=True)
+        hv = torch.empty(en, dtype=torch.uint64, pin_memory=True)
+        ok = torch.empty(en, dtype=torch.uint64, pin_memory=True)
+        ov = torch.empty(en, dtype=torch.uint64, pin_memory=True)
+        hk.copy_(src.keys[:en])
+        hv.copy_(src.values[:en])
+        p_e = S.TuningParams.for_input(en)
+        del work
+        torch.cuda.empty_cache()
+        ts = []
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            torch.cuda.synchronize()
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            data = S.RecordArray(hk, hv)                 # H2D through the public API
+            S.semisort(data, adp, "eq", p_e)
+            ok.copy_(data.keys, non_blocking=True)       # D2H of the result
+            ov.copy_(data.values, non_blocking=True)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1))
+            del data
+        e_ms = sum(ts) / len(ts)
+        e2e = {"value": en / (e_ms / 1e3) / 1e9, "unit": "Grecords/s", "h2d_bytes_per_step": 16 * en,
+               "d2h_bytes_per_step": 16 * en, "ms_per_step": e_ms, "n": en,
+               "path": "RecordArray(pinned host tensors) -> semisort -> copy to pinned host"}
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cpu = cpu_baseline(args.cpu_n)
+
+    if rank == 0:
+        line = {
+            "metric": "semisort Grecords/s (n=1e9 u64 k/v, Zipf 1.2 hashed)",
+            "value": value, "unit": "Grecords/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (device-generated, seeded)",
+            "config": {"workload": "c2: semisort n=1e9 per GPU, uint64 key/value, Zipf s=1.2 ranks over [1,1e9] "
+                                   "hashed (mix64), value = index",
+                       "n_per_gpu": n, "params": "TuningParams.for_input(n) (reference defaults, seed 1)",
+                       "l2": "input restored from a pristine copy before each step (16 GB write flushes L2)",
+                       "parallelism": f"dp{world}" if world > 1 else "single"},
+            "roofline": {"bound": "hbm", "kernel": "k_distribute (blocked distributing scatter, all levels)",
+                         "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                         "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
+                         "peak_kind": peak_kind,
+                         "bytes_model": "32 B per bucketed record (read 16 B + write 16 B)"},
+            "step_roofline": {"bytes_per_record": B_ALG, "achieved_gbs": step_achieved, "peak": peak_gbs,
+                              "frac_of_measured": step_achieved / peak_gbs,
+                              "frac_of_nominal_8tbs": step_achieved * 1e9 / NOMINAL_HBM},
+            "phase_ms_per_step": {k: v / steps for k, v in tel.phase_ms.items()},
+            "levels": tel.levels / steps, "gpu_launches": launches,
+            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "validated": valid,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -278,7 +278,7 @@ def _counts(data: RecordArray, ids, params: TuningParams, n_buckets: int, heavy,
     ident = device_identity_flag(adapter) if adapter is not None else 0
     pc = params.as_c()
     wsb = _lib.lib().ss_phase_workspace_bytes(n, kb, 0, C.byref(pc))
-    wsb += rows * max(n_buckets, 1) * 12
+    wsb += (rows + 2) * (max(n_buckets, 1) + 2) * 24 + (1 << 20)
     ws = _workspace(wsb, dev)
     keys_ptr = data.keys.data_ptr() if data is not None else ids.data_ptr()
     _lib.check(_lib.lib().ss_count_matrix(keys_ptr, _ptr(ids), n, kb, ident, C.byref(pc), depth, _ptr(hk), nh,
@@ -338,7 +338,7 @@ def _distribute(src: RecordArray, dst: RecordArray, ids, prefix, params: TuningP
     ident = device_identity_flag(adapter) if adapter is not None else 0
     pc = params.as_c()
     wsb = _lib.lib().ss_phase_workspace_bytes(n, kb, vb, C.byref(pc)) + \
-        params.num_subarrays(n) * max(n_buckets, 1) * 12
+        (params.num_subarrays(n) + 2) * (max(n_buckets, 1) + 2) * 24 + (1 << 20)
     ws = _workspace(wsb, dev)
     _lib.check(_lib.lib().ss_distribute(src.keys.data_ptr(), _ptr(src.values), dst.keys.data_ptr(),
                                         _ptr(dst.values), _ptr(ids), n, kb, vb, ident, C.byref(pc), depth,

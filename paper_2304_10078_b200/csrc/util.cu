@@ -173,7 +173,8 @@ __global__ void k_count_distinct(const K* __restrict__ keys, uint64_t n, uint64_
         continue;
       }
       while (o == 1) o = atomicAdd(&occ[s], 0u);
-      if (tk[s] == k) break;
+      // the key was published by another SM: read it from L2, not a stale L1 line
+      if (__ldcg(&tk[s]) == k) break;
       s = (s + 1) & mask;
     }
   }
