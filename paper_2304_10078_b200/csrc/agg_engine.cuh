@@ -297,7 +297,7 @@ struct AggEngine {
     d_X = a.take<uint64_t>(max_rows * stride);
     d_P = a.take<uint64_t>(max_grps * stride);
     d_off = a.take<uint64_t>(max_nodes * (stride + 1));
-    d_ccnt = a.take<uint32_t>(max_nodes * 3);
+    d_ccnt = a.take<uint32_t>(max_nodes * 4);
     d_misc = a.take<uint64_t>(8);
     d_leaf_s = a.take<Leaf>(max_leaves);
     d_leaf_g = a.take<Leaf>(max_leaves);
@@ -442,11 +442,7 @@ struct AggEngine {
     tr.launched(6);
 
     tr.begin(kPhDistribute);
-    const size_t dsm = dist_smem_bytes(stride, sizeof(K), ValTraits<V>::bytes);
-    auto dkern = k_distribute<K, V, KeyBuckets>;
-    SS_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-    dkern<<<nwork, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets, bf);
-    check_launch();
+    launch_distribute<K, V, KeyBuckets>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets, bf, st);
     tr.launched();
 
     tr.begin(kPhCopy);
@@ -460,12 +456,12 @@ struct AggEngine {
 
     tr.begin(kPhChildren);
     SS_CUDA(cudaMemsetAsync(d_misc, 0, 5 * sizeof(uint64_t), st));
-    k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff, kLeafSmemMax,
-                                         d_ccnt);
+    const LeafClasses lcls{0, kLeafSmemMax, P.base_case_cutoff};
+    k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt);
     k_children_scan<<<1, 1024, 0, st>>>(d_ccnt, nn, d_misc);
-    k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff, kLeafSmemMax,
-                                        d_ccnt, d_nbase, rounds_per_hash(P.light_bits), d_leaf_s, d_leaf_g, d_next,
-                                        d_misc + 3);
+    k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt, d_nbase,
+                                        rounds_per_hash(P.light_bits), d_leaf_s, d_leaf_s, d_leaf_g, d_next,
+                                        d_misc + 4);
     check_launch();
     tr.launched(3);
     tr.end();
@@ -476,7 +472,7 @@ struct AggEngine {
     SS_CUDA(cudaMemcpyAsync(cur.data(), d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaMemcpyAsync(ntot.data(), d_ntot, nn * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaStreamSynchronize(st));
-    const uint64_t n_s = misc[0], n_g = misc[1], n_next = misc[2];
+    const uint64_t n_s = misc[1], n_g = misc[2], n_next = misc[3];
     std::vector<Node> next(n_next);
     if (n_next) {
       SS_CUDA(cudaMemcpyAsync(next.data(), d_next, n_next * sizeof(Node), cudaMemcpyDeviceToHost, st));

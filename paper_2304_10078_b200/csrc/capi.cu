@@ -178,7 +178,7 @@ __global__ void k_assign_ids(const K* __restrict__ keys, uint64_t n, const uint6
                              uint32_t n_heavy, LightCfg lc, int identity, uint32_t n_light,
                              int32_t* __restrict__ out) {
   __shared__ HeavySmem tab;
-  heavy_build(tab, heavy, n_heavy);
+  heavy_build(tab, heavy, n_heavy, identity != 0);
   __syncthreads();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -543,7 +543,7 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
     Params P = to_params(params, n, false);
     cudaStream_t st = as_stream(stream);
     if (n == 0) return;
-    if (n_buckets > 4600) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
+    if (n_buckets >= kSentinel) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
     PhasePlan pp{};
     Arena a(workspace, workspace_bytes);
     pp.carve(a, n, std::max<uint32_t>(n_buckets, P.light_buckets + P.max_heavy), P, key_bytes);
@@ -558,14 +558,11 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
     check_launch();
     const uint32_t nw = static_cast<uint32_t>(work.size());
     dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
-      const size_t dsm = dist_smem_bytes(pp.stride, sizeof(K), ValTraits<V>::bytes);
       if (ids) {
         IdBuckets bf{static_cast<const int32_t*>(ids), n_buckets};
-        auto kern = k_distribute<K, V, IdBuckets>;
-        SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-        kern<<<nw, kDistThreads, dsm, st>>>(static_cast<const K*>(src_keys), static_cast<const V*>(src_values),
-                                            static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
-                                            pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf);
+        launch_distribute<K, V, IdBuckets>(static_cast<const K*>(src_keys), static_cast<const V*>(src_values),
+                                           static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
+                                           pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf, st);
       } else {
         KeyBuckets bf{};
         bf.heavy = pp.d_heavy;
@@ -573,13 +570,10 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
         bf.n_light = P.light_buckets;
         bf.light_bits = P.light_bits;
         bf.identity = identity;
-        auto kern = k_distribute<K, V, KeyBuckets>;
-        SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-        kern<<<nw, kDistThreads, dsm, st>>>(static_cast<const K*>(src_keys), static_cast<const V*>(src_values),
+        launch_distribute<K, V, KeyBuckets>(static_cast<const K*>(src_keys), static_cast<const V*>(src_values),
                                             static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
-                                            pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf);
+                                            pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf, st);
       }
-      check_launch();
     });
     SS_CUDA(cudaStreamSynchronize(st));
   });

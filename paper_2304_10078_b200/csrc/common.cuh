@@ -92,31 +92,41 @@ struct LightCfg {
 constexpr int kHeavySlots = 1024;   // >= 2 * max_heavy (500); power of two
 constexpr int kMaxHeavyDevice = 512;
 
+// Open-addressing table keyed by the heavy key; the home slot is the top 10
+// bits of the key's (mixed) hash, and a 1024-bit home bitmap lets the
+// common light record leave after one shared-memory word test.
 struct HeavySmem {
   uint64_t keys[kHeavySlots];
   unsigned short ids[kHeavySlots];
+  uint32_t home_bits[kHeavySlots / 32];
 };
 
-__device__ __forceinline__ uint32_t heavy_home(uint64_t key) {
-  return static_cast<uint32_t>((key * kGamma) >> 54) & (kHeavySlots - 1);
+// 64-bit hash used for the table home slot (mix64 for identity keys too).
+__device__ __forceinline__ uint64_t heavy_hash(uint64_t key, uint64_t h, bool identity) {
+  return identity ? key * kGamma : h;
 }
+__device__ __forceinline__ uint32_t heavy_home_of(uint64_t hh) { return static_cast<uint32_t>(hh >> 54); }
 
 // Cooperative parallel build; caller must __syncthreads() afterwards.
-__device__ __forceinline__ void heavy_build(HeavySmem& t, const uint64_t* heavy, uint32_t n_heavy) {
+__device__ __forceinline__ void heavy_build(HeavySmem& t, const uint64_t* heavy, uint32_t n_heavy, bool identity) {
   for (int s = threadIdx.x; s < kHeavySlots; s += blockDim.x) t.ids[s] = 0xFFFF;
+  for (int s = threadIdx.x; s < kHeavySlots / 32; s += blockDim.x) t.home_bits[s] = 0;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n_heavy; i += blockDim.x) {
-    uint64_t k = heavy[i];
-    uint32_t s = heavy_home(k);
+    const uint64_t k = heavy[i];
+    const uint32_t home = heavy_home_of(heavy_hash(k, identity ? k : mix64(k), identity));
+    atomicOr(&t.home_bits[home >> 5], 1u << (home & 31));
+    uint32_t s = home;
     while (atomicCAS(&t.ids[s], static_cast<unsigned short>(0xFFFF), static_cast<unsigned short>(i)) != 0xFFFF)
       s = (s + 1) & (kHeavySlots - 1);
     t.keys[s] = k;
   }
 }
 
-// Returns the heavy slot of key or -1.
-__device__ __forceinline__ int heavy_find(const HeavySmem& t, uint64_t key) {
-  uint32_t s = heavy_home(key);
+// Returns the heavy slot of key (with 64-bit hash h) or -1.
+__device__ __forceinline__ int heavy_find(const HeavySmem& t, uint64_t key, uint64_t h, bool identity) {
+  uint32_t s = heavy_home_of(heavy_hash(key, h, identity));
+  if (!(t.home_bits[s >> 5] & (1u << (s & 31)))) return -1;
   while (true) {
     uint16_t id = t.ids[s];
     if (id == 0xFFFF) return -1;
@@ -129,12 +139,42 @@ __device__ __forceinline__ int heavy_find(const HeavySmem& t, uint64_t key) {
 template <typename K>
 __device__ __forceinline__ uint32_t bucket_of(K key, const HeavySmem& t, uint32_t n_heavy,
                                               const LightCfg& lc, bool identity, uint32_t n_light) {
-  uint64_t k = static_cast<uint64_t>(key);
+  const uint64_t k = static_cast<uint64_t>(key);
+  const uint64_t h = identity ? k : mix64(k);
   if (n_heavy) {
-    int h = heavy_find(t, k);
-    if (h >= 0) return n_light + static_cast<uint32_t>(h);
+    int hv = heavy_find(t, k, h, identity);
+    if (hv >= 0) return n_light + static_cast<uint32_t>(hv);
   }
-  return lc.id(identity ? k : mix64(k));
+  return lc.id(h);
+}
+
+// Lanes of `active` whose value equals this lane's, from `bits` ballots
+// (a multisplit peer mask without MATCH.ANY, whose ADU issue cost is ~57
+// SM cycles per warp instruction on sm_100).  All 32 lanes must call it.
+__device__ __forceinline__ uint32_t ballot_peers(uint32_t v, uint32_t active, int bits) {
+  uint32_t m = active;
+  for (int j = 0; j < bits; ++j) {
+    const uint32_t bit = (v >> j) & 1u;
+    const uint32_t b = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? b : ~b;
+  }
+  return m;
+}
+
+template <int BITS>
+__device__ __forceinline__ uint32_t ballot_peers_t(uint32_t v, uint32_t active) {
+  uint32_t m = active;
+#pragma unroll
+  for (int j = 0; j < BITS; ++j) {
+    const uint32_t bit = (v >> j) & 1u;
+    const uint32_t b = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? b : ~b;
+  }
+  return m;
+}
+
+__device__ __forceinline__ int bits_for(uint32_t n) {   // ceil(log2(n)), n >= 1
+  return n <= 1 ? 0 : 32 - __clz(n - 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -3,23 +3,30 @@
 // node of a recursion level.
 //
 // * k_count     one CTA per subarray (work item): bucket ids are recomputed
-//               from the key (hash + SMEM heavy table), aggregated per warp
-//               with __match_any_sync and added to SMEM counters; one row of
-//               C is written.  Reads K bytes / record.
+//               from the key (hash + SMEM heavy table with a home-bit
+//               prefilter) and added to SMEM counters; heavy buckets (the
+//               hot ones) are warp-aggregated with ballot peer masks first.
+//               One row of C is written.  Reads K bytes / record.
 // * scan        three small kernels: partial column sums per row group,
 //               per-node bucket-major scan, and the cursor matrix
 //               X[row][b] = out_base + (column-major exclusive prefix).
 // * k_distribute
-//               one CTA per subarray owns its X row as SMEM cursors and walks
-//               the subarray in 2048-record tiles.  Each warp ranks its 256
-//               records in index order (match_any + per-warp u16 histograms),
-//               a per-bucket prefix over warps orders warps, the tile is
-//               staged bucket-sorted in SMEM and written out as contiguous
-//               runs per bucket.  Stability and race freedom come from the
-//               disjoint cursor ranges, never from atomics.
+//               persistent, one 512-thread CTA per SM.  Each CTA walks its
+//               subarrays in 4096-record tiles; tile t+1 streams into a
+//               second shared buffer by TMA bulk copy (cp.async.bulk +
+//               mbarrier) while tile t is ranked.  Ranking is a stable
+//               two-pass 7-bit LSD radix sort of (bucket, index) in shared
+//               memory (ballot peer masks, per-warp digit counts), so the
+//               per-tile cost is O(tile) rather than O(warps x buckets).
+//               Records are then written as contiguous per-bucket runs from
+//               the staged tile at the SMEM cursors of the subarray's X
+//               row.  Stability and race freedom come from the disjoint
+//               cursor ranges, never from atomics deciding order
+//               (SPEC.md:195).
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 #include "types.cuh"
 
 namespace ss {
@@ -40,15 +47,14 @@ struct KeyBuckets {
   LightCfg lc;
   uint32_t n_heavy;
 
-  static constexpr bool kUsesTable = true;
-
   __device__ __forceinline__ void prepare(const Node& nd, uint32_t node_idx, HeavySmem* t) {
     tab = t;
     n_heavy = nd.n_heavy;
     lc = LightCfg::make(nd.depth, light_bits, n_light);
-    heavy_build(*tab, heavy + static_cast<uint64_t>(node_idx) * max_heavy, n_heavy);
+    heavy_build(*tab, heavy + static_cast<uint64_t>(node_idx) * max_heavy, n_heavy, identity != 0);
   }
   __device__ __forceinline__ uint32_t n_buckets() const { return n_light + n_heavy; }
+  __device__ __forceinline__ uint32_t first_hot() const { return n_light; }
   template <typename K>
   __device__ __forceinline__ uint32_t operator()(K key, uint64_t) const {
     return bucket_of(key, *tab, n_heavy, lc, identity != 0, n_light);
@@ -59,9 +65,9 @@ struct KeyBuckets {
 struct IdBuckets {
   const int32_t* ids;      // indexed by absolute source position
   uint32_t nb;
-  static constexpr bool kUsesTable = false;
-  __device__ __forceinline__ void prepare(const Node&, uint32_t, HeavySmem*) {}
+  __device__ __forceinline__ void prepare(const Node&, uint32_t, HeavySmem*) { __syncthreads(); }
   __device__ __forceinline__ uint32_t n_buckets() const { return nb; }
+  __device__ __forceinline__ uint32_t first_hot() const { return nb; }
   template <typename K>
   __device__ __forceinline__ uint32_t operator()(K, uint64_t pos) const {
     return static_cast<uint32_t>(ids[pos]);
@@ -75,6 +81,19 @@ struct IdBuckets {
 constexpr int kCountThreads = 256;
 constexpr int kCountItems = 8;
 
+// Adds one record per valid lane to cnt[b].  Light buckets (< hot) are
+// spread and go straight to shared atomics; hot (heavy) buckets are
+// aggregated per warp with ballot peer masks over `hot_bits` bits first.
+__device__ __forceinline__ void count_add(uint32_t* cnt, uint32_t b, bool valid, uint32_t hot, int hot_bits) {
+  const bool is_hot = valid && b >= hot;
+  if (valid && !is_hot) atomicAdd(&cnt[b], 1u);
+  const uint32_t hot_lanes = __ballot_sync(0xffffffffu, is_hot);
+  if (hot_lanes) {
+    const uint32_t peers = ballot_peers(is_hot ? b - hot : 0u, hot_lanes, hot_bits);
+    if (is_hot && lane_id() == __ffs(peers) - 1) atomicAdd(&cnt[b], static_cast<uint32_t>(__popc(peers)));
+  }
+}
+
 template <typename K, typename BF>
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_work,
@@ -86,6 +105,8 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
     const Node nd = nodes[wk.node];
     bf.prepare(nd, wk.node, &tab);
     const uint32_t nb = bf.n_buckets();
+    const uint32_t hot = bf.first_hot();
+    const int hot_bits = bits_for(nb > hot ? nb - hot : 1);
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
     __syncthreads();
     const uint64_t begin = wk.begin;
@@ -99,14 +120,10 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
-        uint32_t i = base + k * kCountThreads + threadIdx.x;
-        bool valid = i < len;
-        uint32_t act = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-          uint32_t b = bf(keys[k], begin + i);
-          uint32_t peers = __match_any_sync(act, b);
-          if (lane_id() == __ffs(peers) - 1) atomicAdd(&cnt[b], __popc(peers));
-        }
+        const uint32_t i = base + k * kCountThreads + threadIdx.x;
+        const bool valid = i < len;
+        const uint32_t b = valid ? bf(keys[k], begin + i) : 0u;
+        count_add(cnt, b, valid, hot, hot_bits);
       }
     }
     __syncthreads();
@@ -212,164 +229,266 @@ __global__ void k_write_X(const CT* __restrict__ C, const Node* __restrict__ nod
 }
 
 // ---------------------------------------------------------------------------
-// the stable scatter
+// the stable scatter (TMA-pipelined, radix-ranked)
 // ---------------------------------------------------------------------------
 
-constexpr int kDistThreads = 256;
+constexpr int kDistThreads = 512;
 constexpr int kDistWarps = kDistThreads / 32;
-constexpr int kDistItems = 8;
-constexpr int kDistTile = kDistThreads * kDistItems;     // 2048 records
+constexpr int kRadixBits = 7;
+constexpr int kRadixBins = 1 << kRadixBits;
+constexpr uint32_t kIdxBits = 12;                 // tile index bits (tile <= 4096)
+constexpr uint32_t kSentinel = (1u << (2 * kRadixBits)) - 1;   // bucket sorting last
 
-// Dynamic SMEM layout (bytes) for a stride.
-__host__ __device__ inline size_t dist_smem_bytes(uint32_t stride, int key_bytes, int val_bytes) {
-  size_t s2 = (stride + 1) & ~1u;
-  return s2 * kDistWarps * 2          // per-warp u16 histograms
-         + static_cast<size_t>(stride) * 8   // cursors
-         + static_cast<size_t>(stride) * 4   // tile offsets
-         + static_cast<size_t>(kDistTile) * (key_bytes + val_bytes + 2) + 64;
+template <typename K, typename V>
+struct DistCfg {
+  static constexpr int kValBytes = ValTraits<V>::bytes;
+  static constexpr int kTile = (sizeof(K) + kValBytes) <= 16 ? 4096 : 2048;
+  static constexpr int kItems = kTile / kDistThreads;
+  static constexpr int kPadK = 16 / sizeof(K);
+  static constexpr int kPadV = kValBytes ? (16 / kValBytes > 0 ? 16 / kValBytes : 1) : 0;
+  static constexpr size_t kBufK = (static_cast<size_t>(kTile) + kPadK) * sizeof(K);
+  static constexpr size_t kBufV = kValBytes ? (static_cast<size_t>(kTile) + kPadV) * kValBytes : 0;
+  static size_t smem_bytes(uint32_t stride) {
+    auto up16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    return 2 * up16(kBufK) + 2 * up16(kBufV) + 2 * kTile * 4 + up16(static_cast<size_t>(stride) * 8) +
+           up16(static_cast<size_t>(stride) * 4) + kDistWarps * kRadixBins * 4 + 64;
+  }
+};
+
+template <typename K, typename V>
+__host__ inline size_t dist_smem_bytes_t(uint32_t stride) { return DistCfg<K, V>::smem_bytes(stride); }
+
+// One stable LSD pass over the tile: entries e[k] sit at logical positions
+// w*(32*ITEMS) + k*32 + lane; digit = (e >> shift) & 127.  Writes the
+// entries to `out` ordered by (digit, logical position).
+template <int ITEMS>
+__device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* out,
+                                           uint32_t* red) {
+  const int w = warp_id(), lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  uint32_t* mine = dh + w * kRadixBins;
+  for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) dh[i] = 0;
+  __syncthreads();
+  uint32_t rk[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
+    const uint32_t peers = ballot_peers_t<kRadixBits>(d, 0xffffffffu);
+    const uint32_t base = mine[d];
+    __syncwarp();
+    if (lane == 31 - __clz(peers)) mine[d] = base + __popc(peers);
+    rk[k] = base + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive scan in (digit, warp) order: 4 consecutive entries per thread
+  constexpr int kEntries = kDistWarps * kRadixBins;
+  constexpr int kPer = kEntries / kDistThreads;
+  uint32_t v[kPer], s = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int j = threadIdx.x * kPer + q;          // j = d * kDistWarps + w
+    v[q] = dh[(j % kDistWarps) * kRadixBins + j / kDistWarps];
+    s += v[q];
+  }
+  uint32_t tot;
+  uint32_t run = block_excl_scan<uint32_t>(s, red, tot);
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int j = threadIdx.x * kPer + q;
+    dh[(j % kDistWarps) * kRadixBins + j / kDistWarps] = run;
+    run += v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
+    out[mine[d] + rk[k]] = e[k];
+  }
+  __syncthreads();
 }
 
 template <typename K, typename V, typename BF>
-__global__ void __launch_bounds__(kDistThreads)
+__global__ void __launch_bounds__(kDistThreads, 1)
 k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__ dk, V* __restrict__ dv,
              const Work* __restrict__ work, uint32_t n_work, const Node* __restrict__ nodes,
              const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below, BF bf) {
-  constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  using Cfg = DistCfg<K, V>;
+  constexpr bool kHasV = Cfg::kValBytes > 0;
+  constexpr int T = Cfg::kTile;
+  constexpr int ITEMS = Cfg::kItems;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ HeavySmem tab;
   __shared__ uint32_t red[33];
-  const uint32_t s2 = (stride + 1) & ~1u;
-  uint64_t* cursor = reinterpret_cast<uint64_t*>(smem);
-  K* stage_k = reinterpret_cast<K*>(cursor + stride);
-  V* stage_v = reinterpret_cast<V*>(stage_k + kDistTile);
-  uint32_t* toff = reinterpret_cast<uint32_t*>(kHasV ? reinterpret_cast<unsigned char*>(stage_v + kDistTile)
-                                                     : reinterpret_cast<unsigned char*>(stage_v));
-  uint16_t* whist = reinterpret_cast<uint16_t*>(toff + stride);
-  uint16_t* sb = whist + s2 * kDistWarps;
+  __shared__ __align__(8) uint64_t bars[2];
+
+  auto up16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+  unsigned char* p = smem;
+  K* bufK[2];
+  V* bufV[2];
+  bufK[0] = reinterpret_cast<K*>(p); p += up16(Cfg::kBufK);
+  bufK[1] = reinterpret_cast<K*>(p); p += up16(Cfg::kBufK);
+  bufV[0] = reinterpret_cast<V*>(p); p += up16(Cfg::kBufV);
+  bufV[1] = reinterpret_cast<V*>(p); p += up16(Cfg::kBufV);
+  uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
+  uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
+  uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += up16(static_cast<size_t>(stride) * 8);
+  uint32_t* toff = reinterpret_cast<uint32_t*>(p); p += up16(static_cast<size_t>(stride) * 4);
+  uint32_t* dh = reinterpret_cast<uint32_t*>(p);
 
   const int w = warp_id(), lane = lane_id();
-  const uint32_t lt = lanemask_lt();
 
-  for (uint32_t wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
-    const Work wk = work[wi];
-    const Node nd = nodes[wk.node];
-    bf.prepare(nd, wk.node, &tab);
-    uint32_t nb = bf.n_buckets();
-    if (nb > keep_below) nb = keep_below;
-    // thread-owned contiguous bucket range (for the per-tile scans)
-    const uint32_t per = (nb + kDistThreads - 1) / kDistThreads;
-    const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
-    const uint64_t* xrow = X + wk.row * stride;
-    for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) cursor[b] = xrow[b];
-    for (uint32_t i = threadIdx.x; i < s2 * kDistWarps / 2; i += kDistThreads)
-      reinterpret_cast<uint32_t*>(whist)[i] = 0;
-    __syncthreads();
+  // tile iterator over this CTA's work items
+  struct It {
+    uint32_t wi;
+    uint32_t tb;
+  };
+  auto first_it = [&](uint32_t wi0) {
+    It it{wi0, 0};
+    while (it.wi < n_work && work[it.wi].len == 0) it.wi += gridDim.x;
+    return it;
+  };
+  auto next_it = [&](It it) {
+    it.tb += T;
+    if (it.tb >= work[it.wi].len) it = first_it(it.wi + gridDim.x);
+    return it;
+  };
+  auto issue = [&](It it, int buf) {   // one thread
+    const Work wk = work[it.wi];
+    const uint64_t begin = wk.begin + it.tb;
+    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - it.tb);
+    uint32_t bytes = span_body_bytes(sk, begin, cnt);
+    if constexpr (kHasV) bytes += span_body_bytes(sv, begin, cnt);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bars[buf], bytes);
+    stage_span(bufK[buf], sk, begin, cnt, &bars[buf]);
+    if constexpr (kHasV) stage_span(bufV[buf], sv, begin, cnt, &bars[buf]);
+  };
 
-    const uint64_t begin = wk.begin;
-    const uint32_t len = wk.len;
-    for (uint32_t tb = 0; tb < len; tb += kDistTile) {
-      // -- load (warp-striped: warp w owns tile positions [w*256, w*256+256))
-      K key[kDistItems];
-      V val[kDistItems];
-      uint32_t bkt[kDistItems], rk[kDistItems];
-#pragma unroll
-      for (int k = 0; k < kDistItems; ++k) {
-        uint32_t i = tb + w * (32 * kDistItems) + k * 32 + lane;
-        bool valid = i < len;
-        key[k] = valid ? ldg_key(sk, begin + i) : K(0);
-        if constexpr (kHasV) { if (valid) val[k] = sv[begin + i]; }
-        bkt[k] = kNoBucket;
-        if (valid) {
-          uint32_t b = bf(key[k], begin + i);
-          if (b < nb) bkt[k] = b;
-        }
-      }
-      // -- per-warp stable ranks
-      uint16_t* wh = whist + w * s2;
-#pragma unroll
-      for (int k = 0; k < kDistItems; ++k) {
-        const bool valid = bkt[k] != kNoBucket;
-        const uint32_t act = __ballot_sync(0xffffffffu, valid);
-        uint32_t peers = 0, base = 0;
-        if (valid) {
-          peers = __match_any_sync(act, bkt[k]);
-          base = wh[bkt[k]];
-        }
-        __syncwarp();
-        if (valid && lane == 31 - __clz(peers)) wh[bkt[k]] = static_cast<uint16_t>(base + __popc(peers));
-        rk[k] = base + __popc(peers & lt);
-        __syncwarp();
-      }
-      __syncthreads();
-      // -- per-bucket prefix over warps, then bucket-major tile offsets
-      uint32_t local = 0;
-      for (uint32_t b = b0; b < b1; ++b) {
-        uint32_t run = 0;
-#pragma unroll
-        for (int ww = 0; ww < kDistWarps; ++ww) {
-          uint32_t t = whist[ww * s2 + b];
-          whist[ww * s2 + b] = static_cast<uint16_t>(run);
-          run += t;
-        }
-        toff[b] = run;           // temporarily the bucket's tile count
-        local += run;
-      }
-      uint32_t tile_total;
-      uint32_t at = block_excl_scan<uint32_t>(local, red, tile_total);
-      for (uint32_t b = b0; b < b1; ++b) {
-        uint32_t c = toff[b];
-        toff[b] = at;
-        at += c;
-      }
-      __syncthreads();
-      // -- stage bucket-sorted
-#pragma unroll
-      for (int k = 0; k < kDistItems; ++k) {
-        if (bkt[k] == kNoBucket) continue;
-        uint32_t s = toff[bkt[k]] + whist[w * s2 + bkt[k]] + rk[k];
-        stage_k[s] = key[k];
-        if constexpr (kHasV) stage_v[s] = val[k];
-        sb[s] = static_cast<uint16_t>(bkt[k]);
-      }
-      __syncthreads();
-      // -- write contiguous runs
-      for (uint32_t s = threadIdx.x; s < tile_total; s += kDistThreads) {
-        const uint32_t b = sb[s];
-        const uint64_t d = cursor[b] + (s - toff[b]);
-        dk[d] = stage_k[s];
-        if constexpr (kHasV) dv[d] = stage_v[s];
-      }
-      __syncthreads();
-      // -- advance cursors, clear histograms
-      for (uint32_t b = b0; b < b1; ++b) {
-        uint32_t next = (b + 1 < nb) ? toff[b + 1] : tile_total;
-        cursor[b] += next - toff[b];
-      }
-      for (uint32_t i = threadIdx.x; i < s2 * kDistWarps / 2; i += kDistThreads)
-        reinterpret_cast<uint32_t*>(whist)[i] = 0;
-      __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  It cur = first_it(blockIdx.x);
+  if (cur.wi >= n_work) return;
+  if (threadIdx.x == 0) issue(cur, 0);
+  uint32_t q = 0;
+  uint32_t nb = 0;
+  while (cur.wi < n_work) {
+    const int buf = q & 1;
+    const It nxt = next_it(cur);
+    if (threadIdx.x == 0 && nxt.wi < n_work) issue(nxt, buf ^ 1);
+    const Work wk = work[cur.wi];
+    if (cur.tb == 0) {   // new subarray: its node's table and X row
+      const Node nd = nodes[wk.node];
+      bf.prepare(nd, wk.node, &tab);
+      nb = min(bf.n_buckets(), keep_below);
+      const uint64_t* xrow = X + wk.row * stride;
+      for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) cursor[b] = xrow[b];
     }
+    const uint64_t begin = wk.begin + cur.tb;
+    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - cur.tb);
+    const uint32_t shK = Span16<K>(sk, begin, cnt).sh;
+    uint32_t shV = 0;
+    if constexpr (kHasV) shV = Span16<V>(sv, begin, cnt).sh;
+    mbar_wait(&bars[buf], (q >> 1) & 1);
+    __syncthreads();   // head/tail elements, cursors and the table are visible
+
+    // bucket of every record -> (bucket << 12) | tile index
+    uint32_t e[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
+      uint32_t b = kSentinel;
+      if (i < cnt) {
+        b = bf(bufK[buf][i + shK], begin + i);
+        if (b >= nb) b = kSentinel;
+      }
+      e[k] = (b << kIdxBits) | i;
+    }
+    radix_pass<ITEMS>(e, kIdxBits, dh, srtA, red);
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
+    radix_pass<ITEMS>(e, kIdxBits + kRadixBits, dh, srtB, red);
+
+    // run starts -> per-bucket tile offsets
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t s = threadIdx.x + k * kDistThreads;
+      const uint32_t b = srtB[s] >> kIdxBits;
+      if (b != kSentinel && (s == 0 || (srtB[s - 1] >> kIdxBits) != b)) toff[b] = s;
+    }
+    __syncthreads();
+    // contiguous per-bucket runs out of the staged tile
+    bool run_end[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t s = threadIdx.x + k * kDistThreads;
+      const uint32_t ent = srtB[s];
+      const uint32_t b = ent >> kIdxBits;
+      run_end[k] = false;
+      if (b == kSentinel) continue;
+      const uint32_t i = ent & ((1u << kIdxBits) - 1);
+      const uint64_t d = cursor[b] + (s - toff[b]);
+      dk[d] = bufK[buf][i + shK];
+      if constexpr (kHasV) dv[d] = bufV[buf][i + shV];
+      run_end[k] = (s + 1 == static_cast<uint32_t>(T)) || ((srtB[s + 1] >> kIdxBits) != b);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      if (!run_end[k]) continue;
+      const uint32_t s = threadIdx.x + k * kDistThreads;
+      const uint32_t b = srtB[s] >> kIdxBits;
+      cursor[b] += s + 1 - toff[b];
+    }
+    __syncthreads();   // buffer `buf` may be refilled; cursors final for the next tile
+    cur = nxt;
+    ++q;
   }
 }
 
 // ---------------------------------------------------------------------------
-// heavy copy-back S -> A (core.py:478-482)
+// heavy copy-back S -> A (core.py:478-482), vectorised when aligned
 // ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ void copy_span(T* __restrict__ dst, const T* __restrict__ src, uint64_t lo, uint64_t hi,
+                                          uint64_t tid, uint64_t nthreads) {
+  if (hi <= lo) return;
+  // 16-byte vectors when src and dst share alignment
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src + lo), b = reinterpret_cast<uintptr_t>(dst + lo);
+  if (sizeof(T) < 16 && ((a ^ b) & 15) == 0) {
+    constexpr uint64_t per = 16 / sizeof(T);
+    uint64_t head = ((16 - (a & 15)) & 15) / sizeof(T);
+    if (head > hi - lo) head = hi - lo;
+    for (uint64_t i = lo + tid; i < lo + head; i += nthreads) dst[i] = src[i];
+    const uint64_t v0 = lo + head, nv = (hi - v0) / per;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + v0);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + v0);
+    for (uint64_t i = tid; i < nv; i += nthreads) d4[i] = s4[i];
+    for (uint64_t i = v0 + nv * per + tid; i < hi; i += nthreads) dst[i] = src[i];
+  } else {
+    for (uint64_t i = lo + tid; i < hi; i += nthreads) dst[i] = src[i];
+  }
+}
 
 template <typename K, typename V>
 __global__ void k_copy_heavy(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__ dk,
                              V* __restrict__ dv, const Node* __restrict__ nodes, uint32_t n_nodes,
                              const uint64_t* __restrict__ off, uint32_t stride, uint32_t n_light) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint32_t j = blockIdx.y; j < n_nodes; j += gridDim.y) {
     const Node nd = nodes[j];
     const uint64_t h0 = nd.lo + off[static_cast<uint64_t>(j) * (stride + 1) + n_light];
     const uint64_t h1 = nd.lo + nd.size;
-    for (uint64_t i = h0 + blockIdx.x * blockDim.x + threadIdx.x; i < h1;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-      dk[i] = sk[i];
-      if constexpr (kHasV) dv[i] = sv[i];
-    }
+    copy_span(dk, sk, h0, h1, tid, nth);
+    if constexpr (kHasV) copy_span(dv, sv, h0, h1, tid, nth);
   }
 }
 
@@ -377,84 +496,81 @@ template <typename K, typename V>
 __global__ void k_copy_range(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__ dk,
                              V* __restrict__ dv, uint64_t lo, uint64_t hi) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
-  for (uint64_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    dk[i] = sk[i];
-    if constexpr (kHasV) dv[i] = sv[i];
-  }
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  copy_span(dk, sk, lo, hi, tid, nth);
+  if constexpr (kHasV) copy_span(dv, sv, lo, hi, tid, nth);
 }
 
 // ---------------------------------------------------------------------------
 // children: leaves and next-level nodes (core.py:484-498, aggregate.py:166-170)
 // ---------------------------------------------------------------------------
 
-// Per node: count light buckets by class.  cls: 0 empty, 1 small leaf in
-// SMEM range, 2 small leaf (global path), 3 child node.  With
-// all_nodes != 0 (aggregation), every non-empty bucket is a node() call;
-// small ones are still leaves but classified the same way.
-__device__ __forceinline__ int child_class(uint64_t sz, uint64_t alpha, uint64_t smem_max) {
-  if (sz == 0) return 0;
-  if (sz < alpha) return sz <= smem_max ? 1 : 2;
-  return 3;
-}
+// Leaf size classes: 1 warp leaves (<= t1), 2 SMEM CTA leaves (<= t2),
+// 3 global-scratch CTA leaves (< alpha); 4 = child node (>= alpha).
+struct LeafClasses {
+  uint64_t t1, t2, alpha;
+  __device__ __forceinline__ int of(uint64_t sz) const {
+    if (sz == 0) return 0;
+    if (sz >= alpha) return 4;
+    if (sz <= t1) return 1;
+    return sz <= t2 ? 2 : 3;
+  }
+};
 
 static __global__ void k_children_count(const Node* __restrict__ nodes, uint32_t n_nodes,
-                                 const uint64_t* __restrict__ off, uint32_t stride, uint32_t n_light,
-                                 uint64_t alpha, uint64_t smem_max, uint32_t* __restrict__ counts) {
+                                        const uint64_t* __restrict__ off, uint32_t stride, uint32_t n_light,
+                                        LeafClasses lc, uint32_t* __restrict__ counts) {
   __shared__ uint32_t red[33];
   for (uint32_t j = blockIdx.x; j < n_nodes; j += gridDim.x) {
     const uint64_t* o = off + static_cast<uint64_t>(j) * (stride + 1);
-    uint32_t c1 = 0, c2 = 0, c3 = 0;
+    uint32_t c[4] = {0, 0, 0, 0};
     for (uint32_t b = threadIdx.x; b < n_light; b += blockDim.x) {
-      int c = child_class(o[b + 1] - o[b], alpha, smem_max);
-      c1 += c == 1; c2 += c == 2; c3 += c == 3;
+      int k = lc.of(o[b + 1] - o[b]);
+      if (k) c[k - 1] += 1;
     }
-    uint32_t t1, t2, t3;
-    block_excl_scan<uint32_t>(c1, red, t1);
-    block_excl_scan<uint32_t>(c2, red, t2);
-    block_excl_scan<uint32_t>(c3, red, t3);
-    if (threadIdx.x == 0) {
-      counts[3 * j + 0] = t1;
-      counts[3 * j + 1] = t2;
-      counts[3 * j + 2] = t3;
+    for (int k = 0; k < 4; ++k) {
+      uint32_t t;
+      block_excl_scan<uint32_t>(c[k], red, t);
+      if (threadIdx.x == 0) counts[4 * j + k] = t;
     }
   }
 }
 
-// Exclusive scan of the 3 count columns over nodes (single CTA); totals and
-// the max leaf size land in tot[0..3].
+// Exclusive scan of the 4 count columns over nodes (single CTA); totals in tot[0..3].
 static __global__ void __launch_bounds__(1024)
 k_children_scan(uint32_t* __restrict__ counts, uint32_t n_nodes, uint64_t* __restrict__ tot) {
   __shared__ uint32_t red[33];
-  for (int c = 0; c < 3; ++c) {
+  for (int c = 0; c < 4; ++c) {
     uint32_t carry = 0;
     for (uint32_t base = 0; base < n_nodes; base += blockDim.x) {
       uint32_t j = base + threadIdx.x;
-      uint32_t v = j < n_nodes ? counts[3 * j + c] : 0;
+      uint32_t v = j < n_nodes ? counts[4 * j + c] : 0;
       uint32_t t;
       uint32_t ex = block_excl_scan<uint32_t>(v, red, t);
-      if (j < n_nodes) counts[3 * j + c] = carry + ex;
+      if (j < n_nodes) counts[4 * j + c] = carry + ex;
       carry += t;
     }
     if (threadIdx.x == 0) tot[c] = carry;
   }
 }
 
-// Emit, in (node, bucket) order: SMEM leaves, global leaves, child nodes.
+// Emit, in (node, bucket) order, the three leaf lists and the child nodes.
 // Child depth / stall bookkeeping follows core.py:452-460 (applied to the
 // child here instead of on entry, which is equivalent).
 static __global__ void k_children_emit(const Node* __restrict__ nodes, uint32_t n_nodes,
-                                const uint64_t* __restrict__ off, uint32_t stride, uint32_t n_light,
-                                uint64_t alpha, uint64_t smem_max, const uint32_t* __restrict__ counts,
-                                const uint64_t* __restrict__ child_base, uint32_t rounds,
-                                Leaf* __restrict__ leaf_s, Leaf* __restrict__ leaf_g,
-                                Node* __restrict__ next, uint64_t* __restrict__ max_leaf) {
+                                       const uint64_t* __restrict__ off, uint32_t stride, uint32_t n_light,
+                                       LeafClasses lc, const uint32_t* __restrict__ counts,
+                                       const uint64_t* __restrict__ child_base, uint32_t rounds,
+                                       Leaf* __restrict__ leaf1, Leaf* __restrict__ leaf2, Leaf* __restrict__ leaf3,
+                                       Node* __restrict__ next, uint64_t* __restrict__ max_leaf) {
   __shared__ uint32_t red[33];
   for (uint32_t j = blockIdx.x; j < n_nodes; j += gridDim.x) {
     const Node nd = nodes[j];
     const uint64_t* o = off + static_cast<uint64_t>(j) * (stride + 1);
     const uint64_t base = child_base ? child_base[j] : nd.lo;
-    uint32_t a1 = counts[3 * j + 0], a2 = counts[3 * j + 1], a3 = counts[3 * j + 2];
+    uint32_t a[4];
+    for (int k = 0; k < 4; ++k) a[k] = counts[4 * j + k];
     uint64_t mx = 0;
     for (uint32_t bb = 0; bb < n_light; bb += blockDim.x) {
       const uint32_t b = bb + threadIdx.x;
@@ -463,15 +579,14 @@ static __global__ void k_children_emit(const Node* __restrict__ nodes, uint32_t 
       if (b < n_light) {
         lo = o[b];
         sz = o[b + 1] - lo;
-        c = child_class(sz, alpha, smem_max);
+        c = lc.of(sz);
       }
-      uint32_t t1, t2, t3;
-      uint32_t e1 = block_excl_scan<uint32_t>(c == 1, red, t1);
-      uint32_t e2 = block_excl_scan<uint32_t>(c == 2, red, t2);
-      uint32_t e3 = block_excl_scan<uint32_t>(c == 3, red, t3);
-      if (c == 1) leaf_s[a1 + e1] = Leaf{base + lo, sz};
-      if (c == 2) { leaf_g[a2 + e2] = Leaf{base + lo, sz}; mx = sz > mx ? sz : mx; }
-      if (c == 3) {
+      uint32_t ex[4], t[4];
+      for (int k = 0; k < 4; ++k) ex[k] = block_excl_scan<uint32_t>(c == k + 1, red, t[k]);
+      if (c == 1) leaf1[a[0] + ex[0]] = Leaf{base + lo, sz};
+      if (c == 2) leaf2[a[1] + ex[1]] = Leaf{base + lo, sz};
+      if (c == 3) { leaf3[a[2] + ex[2]] = Leaf{base + lo, sz}; mx = sz > mx ? sz : mx; }
+      if (c == 4) {
         Node ch{};
         ch.lo = base + lo;
         ch.size = sz;
@@ -484,9 +599,9 @@ static __global__ void k_children_emit(const Node* __restrict__ nodes, uint32_t 
         }
         ch.depth = depth;
         ch.stalled = stalled;
-        next[a3 + e3] = ch;
+        next[a[3] + ex[3]] = ch;
       }
-      a1 += t1; a2 += t2; a3 += t3;
+      for (int k = 0; k < 4; ++k) a[k] += t[k];
     }
     if (mx) atomicMax(reinterpret_cast<unsigned long long*>(max_leaf), static_cast<unsigned long long>(mx));
   }

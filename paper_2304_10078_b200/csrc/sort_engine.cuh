@@ -30,6 +30,19 @@ inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
   return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
 }
 
+template <typename K, typename V, typename BF>
+inline void launch_distribute(const K* sk, const V* sv, K* dk, V* dv, const Work* d_work, uint32_t nwork,
+                              const Node* d_nodes, const uint64_t* d_X, uint32_t stride, uint32_t keep_below, BF bf,
+                              cudaStream_t st) {
+  if (!nwork) return;
+  const size_t dsm = dist_smem_bytes_t<K, V>(stride);
+  auto kern = k_distribute<K, V, BF>;
+  SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
+  const uint32_t grid = std::min<uint32_t>(nwork, 148);
+  kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, bf);
+  check_launch();
+}
+
 template <typename K, typename V>
 struct SortEngine {
   static constexpr bool kHasV = ValTraits<V>::bytes > 0;
@@ -60,8 +73,9 @@ struct SortEngine {
   uint64_t* d_off = nullptr;
   uint32_t* d_ccnt = nullptr;
   uint64_t* d_misc = nullptr;
-  Leaf* d_leaf_s = nullptr;
-  Leaf* d_leaf_g = nullptr;
+  Leaf* d_leaf_w = nullptr;   // warp leaves (<= kLeafWarpMax)
+  Leaf* d_leaf_s = nullptr;   // SMEM CTA leaves (<= kLeafSmemMax)
+  Leaf* d_leaf_g = nullptr;   // global-scratch CTA leaves
   uint64_t* d_samp = nullptr;
   uint32_t* d_leafscr = nullptr;
   bool external_scratch = false;
@@ -91,8 +105,9 @@ struct SortEngine {
     d_X = a.take<uint64_t>(max_rows * stride);
     d_P = a.take<uint64_t>(max_grps * stride);
     d_off = a.take<uint64_t>(max_nodes * (stride + 1));
-    d_ccnt = a.take<uint32_t>(max_nodes * 3);
+    d_ccnt = a.take<uint32_t>(max_nodes * 4);
     d_misc = a.take<uint64_t>(8);
+    d_leaf_w = a.take<Leaf>(max_leaves);
     d_leaf_s = a.take<Leaf>(max_leaves);
     d_leaf_g = a.take<Leaf>(max_leaves);
     d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * (2 * s_cap + 2 * pow2_ge(s_cap)));
@@ -102,6 +117,22 @@ struct SortEngine {
   bool src_is_A(int level, bool flip) const { return ((level & 1) == 1) != flip; }
 
   // ---- leaves ---------------------------------------------------------------
+  void run_leaves_warp(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a) {
+    if (!count) return;
+    if (mode == SS_MODE_LT) {
+      run_leaves_global(tr, d_list, count, in_a, nullptr, 0);
+      return;
+    }
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(cdiv(count, kLeafWarpWarps), 148 * 3));
+    const size_t sm = sizeof(WarpLeafSmem<K>) * kLeafWarpWarps;
+    SS_CUDA(cudaFuncSetAttribute(k_leaf_eq_warp<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    k_leaf_eq_warp<K, V><<<grid, kLeafWarpWarps * 32, sm, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v,
+                                                               d_list, static_cast<uint32_t>(count), identity);
+    check_launch();
+    tr.launched();
+    if (tel) tel->leaves_smem += count;
+  }
+
   void run_leaves_smem(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a) {
     if (!count) return;
     if (mode == SS_MODE_LT) {
@@ -142,12 +173,17 @@ struct SortEngine {
   // leaves after a stall / at DEPTH_LIMIT): any size.
   void run_host_leaves(Tracker& tr, const std::vector<Leaf>& leaves, bool in_a) {
     if (leaves.empty()) return;
-    std::vector<Leaf> small, mid, huge;
+    std::vector<Leaf> tiny, small, mid, huge;
     const uint64_t mmax_planned = std::max<uint64_t>(1, std::min<uint64_t>(n, P.base_case_cutoff > 1 ? P.base_case_cutoff - 1 : 1));
     for (const Leaf& l : leaves) {
-      if (l.size <= kLeafSmemMax && mode == SS_MODE_EQ) small.push_back(l);
+      if (l.size <= kLeafWarpMax && mode == SS_MODE_EQ) tiny.push_back(l);
+      else if (l.size <= kLeafSmemMax && mode == SS_MODE_EQ) small.push_back(l);
       else if (l.size <= mmax_planned) mid.push_back(l);
       else huge.push_back(l);
+    }
+    if (!tiny.empty()) {
+      SS_CUDA(cudaMemcpyAsync(d_leaf_w, tiny.data(), tiny.size() * sizeof(Leaf), cudaMemcpyHostToDevice, st));
+      run_leaves_warp(tr, d_leaf_w, tiny.size(), in_a);
     }
     if (!small.empty()) {
       SS_CUDA(cudaMemcpyAsync(d_leaf_s, small.data(), small.size() * sizeof(Leaf), cudaMemcpyHostToDevice, st));
@@ -244,10 +280,7 @@ struct SortEngine {
 
     // blocked distributing
     tr.begin(kPhDistribute);
-    const size_t dsm = dist_smem_bytes(stride, sizeof(K), kHasV ? sizeof(V) : 0);
-    auto dkern = k_distribute<K, V, KeyBuckets>;
-    SS_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-    dkern<<<nwork, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu, bf);
+    launch_distribute<K, V, KeyBuckets>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu, bf, st);
     check_launch();
     tr.launched();
 
@@ -265,14 +298,14 @@ struct SortEngine {
     // children
     tr.begin(kPhChildren);
     SS_CUDA(cudaMemsetAsync(d_misc, 0, 8 * sizeof(uint64_t), st));
-    k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff,
-                                         kLeafSmemMax, d_ccnt);
+    const LeafClasses lcls{mode == SS_MODE_EQ ? kLeafWarpMax : 0, kLeafSmemMax, P.base_case_cutoff};
+    k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt);
     check_launch();
     k_children_scan<<<1, 1024, 0, st>>>(d_ccnt, nn, d_misc);
     check_launch();
-    k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, P.base_case_cutoff,
-                                        kLeafSmemMax, d_ccnt, nullptr, rounds_per_hash(P.light_bits),
-                                        d_leaf_s, d_leaf_g, d_next, d_misc + 3);
+    k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt, nullptr,
+                                        rounds_per_hash(P.light_bits), d_leaf_w, d_leaf_s, d_leaf_g, d_next,
+                                        d_misc + 4);
     check_launch();
     tr.launched(3);
     tr.end();
@@ -281,7 +314,7 @@ struct SortEngine {
     SS_CUDA(cudaMemcpyAsync(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaMemcpyAsync(cur.data(), d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaStreamSynchronize(st));
-    const uint64_t n_s = misc[0], n_g = misc[1], n_next = misc[2];
+    const uint64_t n_w = misc[0], n_s = misc[1], n_g = misc[2], n_next = misc[3];
     std::vector<Node> next(n_next);
     if (n_next) {
       SS_CUDA(cudaMemcpyAsync(next.data(), d_next, n_next * sizeof(Node), cudaMemcpyDeviceToHost, st));
@@ -296,7 +329,7 @@ struct SortEngine {
           tel->matrix_cells_by_level[lvl] += cdiv(nd.size, P.subarray_len) * (P.light_buckets + nd.n_heavy);
         if (from_a) tel->scratch_moves += nd.size;
       }
-      const uint64_t kids = n_s + n_g + n_next;
+      const uint64_t kids = n_w + n_s + n_g + n_next;
       tel->nodes += kids;
       if (kids && static_cast<uint64_t>(lvl + 1) > tel->max_depth) tel->max_depth = lvl + 1;
       tel->levels += 1;
@@ -305,6 +338,7 @@ struct SortEngine {
     // leaves of this level live on the destination side
     const bool leaves_in_a = !from_a;
     tr.begin(kPhLeaves);
+    run_leaves_warp(tr, d_leaf_w, n_w, leaves_in_a);
     run_leaves_smem(tr, d_leaf_s, n_s, leaves_in_a);
     run_leaves_global(tr, d_leaf_g, n_g, leaves_in_a, nullptr, 0);
 

@@ -1,0 +1,89 @@
+// Bulk-async (TMA 1-D) global->shared copies tracked by an mbarrier
+// (cp.async.bulk + mbarrier complete_tx), for the streaming kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace ss {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Orders this thread's prior generic-proxy shared accesses before later
+// async-proxy (bulk copy) accesses.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// Split [begin, begin+cnt) of a T array into an unaligned head, a 16-byte
+// aligned bulk body and a tail.  `sh` is the element shift that makes the
+// body land 16-byte aligned in shared memory (element i of the range is
+// stored at index i + sh of a 16-byte aligned buffer).
+template <typename T>
+struct Span16 {
+  uint32_t sh, head, body;
+  __device__ __forceinline__ Span16(const T* base, uint64_t begin, uint32_t cnt) {
+    constexpr uint32_t per = 16 / sizeof(T) > 0 ? 16 / sizeof(T) : 1;
+    const uint32_t mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(base + begin) & 15u) / sizeof(T));
+    sh = mis;
+    head = mis ? min(per - mis, cnt) : 0;
+    body = ((cnt - head) / per) * per;
+  }
+};
+
+// Issued by one thread: bulk copy of the body (returns its bytes, already
+// armed on `bar` by the caller) plus synchronous head/tail element copies.
+template <typename T>
+__device__ __forceinline__ void stage_span(T* buf, const T* src, uint64_t begin, uint32_t cnt, uint64_t* bar) {
+  Span16<T> sp(src, begin, cnt);
+  if (sp.body) bulk_g2s(buf + sp.sh + sp.head, src + begin + sp.head, sp.body * sizeof(T), bar);
+  for (uint32_t i = 0; i < sp.head; ++i) buf[sp.sh + i] = src[begin + i];
+  for (uint32_t i = sp.head + sp.body; i < cnt; ++i) buf[sp.sh + i] = src[begin + i];
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t span_body_bytes(const T* src, uint64_t begin, uint32_t cnt) {
+  Span16<T> sp(src, begin, cnt);
+  return sp.body * sizeof(T);
+}
+
+}  // namespace ss

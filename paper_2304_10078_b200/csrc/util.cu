@@ -188,9 +188,9 @@ __global__ void k_count_distinct(const K* __restrict__ keys, uint64_t n, uint64_
 struct PartBuckets {
   uint32_t shift;   // 64 - log2(parts); 64 means a single part
   uint32_t nb;
-  static constexpr bool kUsesTable = false;
-  __device__ __forceinline__ void prepare(const Node&, uint32_t, HeavySmem*) {}
+  __device__ __forceinline__ void prepare(const Node&, uint32_t, HeavySmem*) { __syncthreads(); }
   __device__ __forceinline__ uint32_t n_buckets() const { return nb; }
+  __device__ __forceinline__ uint32_t first_hot() const { return nb; }
   template <typename K>
   __device__ __forceinline__ uint32_t operator()(K key, uint64_t) const {
     return shift >= 64 ? 0u : static_cast<uint32_t>(mix64(static_cast<uint64_t>(key)) >> shift);
@@ -380,10 +380,10 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       k_scan_nodes<<<1, 1024, 0, st>>>(pp.d_node, 1, pp.d_P, pp.d_off, pp.stride, 0, 0, parts, nullptr);
       k_write_X<uint32_t, uint64_t><<<nd.n_grps, 256, 0, st>>>(pp.d_C, pp.d_node, pp.d_gn, nd.n_grps, pp.d_P, pp.d_X,
                                                                 pp.stride, 0, 0, parts, nullptr);
-      const size_t dsm = dist_smem_bytes(pp.stride, sizeof(K), ValTraits<V>::bytes);
+      const size_t dsm = dist_smem_bytes_t<K, V>(pp.stride);
       auto kern = k_distribute<K, V, PartBuckets>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-      kern<<<nw, kDistThreads, dsm, st>>>(static_cast<const K*>(keys), static_cast<const V*>(values),
+      kern<<<std::min<uint32_t>(nw, 148), kDistThreads, dsm, st>>>(static_cast<const K*>(keys), static_cast<const V*>(values),
                                           static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
                                           pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf);
     };
