@@ -58,17 +58,12 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, const Work* __r
         uint32_t i = base + k * kCountThreads + threadIdx.x;
         bool valid = i < len;
         uint32_t act = __ballot_sync(0xffffffffu, valid);
+        (void)act;
         if (valid) {
-          uint32_t b = bf(keys[k], begin + i);
-          uint32_t peers = __match_any_sync(act, b);
-          const bool leader = lane_id() == __ffs(peers) - 1;
-          if (leader) atomicAdd(&cnt[b], __popc(peers));
-          if (SUM && b >= nl) {
-            uint64_t v = val_u64(sv[begin + i]);
-            uint64_t s = 0;
-            for (uint32_t m = peers; m; m &= m - 1) s += __shfl_sync(peers, v, __ffs(m) - 1);
-            if (leader) atomicAdd(&hsum[b - nl], static_cast<unsigned long long>(s));
-          }
+          const uint32_t b = bf(keys[k], begin + i);
+          atomicAdd(&cnt[b], 1u);   // shared atomics are ~free on sm_100 (see count_add)
+          if (SUM && b >= nl)
+            atomicAdd(&hsum[b - nl], static_cast<unsigned long long>(val_u64(sv[begin + i])));
         }
       }
     }

@@ -75,6 +75,7 @@ __device__ void leaf_group(const K* rk, uint32_t m, uint32_t cap, bool identity,
     a.T[s] = kEmpty32;
     a.gcnt[s] = 0;
     a.cell[s] = 0;
+    a.gstart[s] = 0;   // peer-mask scratch of the rank pass
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
@@ -96,19 +97,26 @@ __device__ void leaf_group(const K* rk, uint32_t m, uint32_t cap, bool identity,
   }
   __syncthreads();
   if (warp_id() == 0) {
+    // in-order pass: peers of the same group among 32 consecutive records
+    // via atomicOr masks in a.gstart (not yet in use)
     const uint32_t lt = lanemask_lt();
-    const int sbits = bits_for(cap);
     for (uint32_t base = 0; base < m; base += 32) {
       const uint32_t i = base + lane_id();
       const bool valid = i < m;
-      const uint32_t act = __ballot_sync(0xffffffffu, valid);
       const uint32_t s = valid ? a.rslot[i] : 0;
-      const uint32_t peers = ballot_peers(s, act, sbits);
-      uint32_t cnt = 0;
-      if (valid) cnt = a.gcnt[s];
+      if (valid) atomicOr(&a.gstart[s], 1u << lane_id());
+      __syncwarp();
+      uint32_t peers = 0, cnt = 0;
+      if (valid) {
+        peers = a.gstart[s];
+        cnt = a.gcnt[s];
+      }
       __syncwarp();
       if (valid) {
-        if (lane_id() == 31 - __clz(peers)) a.gcnt[s] = cnt + __popc(peers);
+        if (lane_id() == 31 - __clz(peers)) {
+          a.gcnt[s] = cnt + __popc(peers);
+          a.gstart[s] = 0;
+        }
         a.rank[i] = cnt + __popc(peers & lt);
       }
       __syncwarp();
@@ -220,9 +228,9 @@ struct WarpLeafSmem {
   K keys[kLeafWarpMax];
   uint32_t T[kLeafWarpCap];
   uint32_t cell[kLeafWarpCap];
+  uint32_t gstart[kLeafWarpCap];   // also the peer-mask scratch of the rank pass
   uint16_t home[kLeafWarpCap];
   uint16_t gcnt[kLeafWarpCap];
-  uint16_t gstart[kLeafWarpCap];
 };
 
 template <typename K, typename V>
@@ -253,6 +261,7 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       ws.T[s] = kEmpty32;
       ws.cell[s] = 0;
       ws.gcnt[s] = 0;
+      ws.gstart[s] = 0;
     }
     __syncwarp();
     uint32_t slot[kLeafWarpItems];
@@ -278,17 +287,20 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
     }
     __syncwarp();
     // in-order ranks within groups (records i = lane + 32k, k ascending)
-    const int sbits = bits_for(cap);
     uint32_t rank[kLeafWarpItems];
 #pragma unroll
     for (int k = 0; k < kLeafWarpItems; ++k) {
       if (32 * k >= m) { rank[k] = 0; continue; }   // warp-uniform
       const bool valid = lane + 32 * k < m;
-      const uint32_t act = __ballot_sync(0xffffffffu, valid);
-      const uint32_t peers = ballot_peers(slot[k], act, sbits);
+      if (valid) atomicOr(&ws.gstart[slot[k]], 1u << lane);
+      __syncwarp();
+      const uint32_t peers = valid ? ws.gstart[slot[k]] : 0u;
       const uint32_t cnt = valid ? ws.gcnt[slot[k]] : 0u;
       __syncwarp();
-      if (valid && lane == 31u - __clz(peers)) ws.gcnt[slot[k]] = static_cast<uint16_t>(cnt + __popc(peers));
+      if (valid && lane == 31u - __clz(peers)) {
+        ws.gcnt[slot[k]] = static_cast<uint16_t>(cnt + __popc(peers));
+        ws.gstart[slot[k]] = 0;
+      }
       rank[k] = cnt + __popc(peers & lt);
       __syncwarp();
     }

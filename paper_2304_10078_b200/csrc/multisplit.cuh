@@ -4,9 +4,10 @@
 //
 // * k_count     one CTA per subarray (work item): bucket ids are recomputed
 //               from the key (hash + SMEM heavy table with a home-bit
-//               prefilter) and added to SMEM counters; heavy buckets (the
-//               hot ones) are warp-aggregated with ballot peer masks first.
-//               One row of C is written.  Reads K bytes / record.
+//               prefilter) and added to SMEM counters with plain shared
+//               atomics (cheaper on sm_100 than any warp aggregation, see
+//               tools/peers_bench.cu).  One row of C is written.  Reads K
+//               bytes / record.
 // * scan        three small kernels: partial column sums per row group,
 //               per-node bucket-major scan, and the cursor matrix
 //               X[row][b] = out_base + (column-major exclusive prefix).
@@ -16,7 +17,7 @@
 //               second shared buffer by TMA bulk copy (cp.async.bulk +
 //               mbarrier) while tile t is ranked.  Ranking is a stable
 //               two-pass 7-bit LSD radix sort of (bucket, index) in shared
-//               memory (ballot peer masks, per-warp digit counts), so the
+//               memory (atomicOr peer masks, per-warp digit counts), so the
 //               per-tile cost is O(tile) rather than O(warps x buckets).
 //               Records are then written as contiguous per-bucket runs from
 //               the staged tile at the SMEM cursors of the subarray's X
@@ -81,17 +82,12 @@ struct IdBuckets {
 constexpr int kCountThreads = 256;
 constexpr int kCountItems = 8;
 
-// Adds one record per valid lane to cnt[b].  Light buckets (< hot) are
-// spread and go straight to shared atomics; hot (heavy) buckets are
-// aggregated per warp with ballot peer masks over `hot_bits` bits first.
-__device__ __forceinline__ void count_add(uint32_t* cnt, uint32_t b, bool valid, uint32_t hot, int hot_bits) {
-  const bool is_hot = valid && b >= hot;
-  if (valid && !is_hot) atomicAdd(&cnt[b], 1u);
-  const uint32_t hot_lanes = __ballot_sync(0xffffffffu, is_hot);
-  if (hot_lanes) {
-    const uint32_t peers = ballot_peers(is_hot ? b - hot : 0u, hot_lanes, hot_bits);
-    if (is_hot && lane_id() == __ffs(peers) - 1) atomicAdd(&cnt[b], static_cast<uint32_t>(__popc(peers)));
-  }
+// Adds one record per valid lane to cnt[b].  Shared-memory atomicAdd on
+// sm_100 costs ~1.3 SM cycles per warp op even when most lanes hit one hot
+// (heavy) counter (tools/peers_bench.cu), far below any warp aggregation
+// (MATCH.ANY ~53, 7-bit ballot peers ~21), so no aggregation is done.
+__device__ __forceinline__ void count_add(uint32_t* cnt, uint32_t b, bool valid, uint32_t, int) {
+  if (valid) atomicAdd(&cnt[b], 1u);
 }
 
 template <typename K, typename BF>
@@ -251,7 +247,7 @@ struct DistCfg {
   static size_t smem_bytes(uint32_t stride) {
     auto up16 = [](size_t x) { return (x + 15) & ~size_t(15); };
     return 2 * up16(kBufK) + 2 * up16(kBufV) + 2 * kTile * 4 + up16(static_cast<size_t>(stride) * 8) +
-           up16(static_cast<size_t>(stride) * 4) + kDistWarps * kRadixBins * 4 + 64;
+           up16(static_cast<size_t>(stride) * 4) + 2 * kDistWarps * kRadixBins * 4 + 64;
   }
 };
 
@@ -261,22 +257,31 @@ __host__ inline size_t dist_smem_bytes_t(uint32_t stride) { return DistCfg<K, V>
 // One stable LSD pass over the tile: entries e[k] sit at logical positions
 // w*(32*ITEMS) + k*32 + lane; digit = (e >> shift) & 127.  Writes the
 // entries to `out` ordered by (digit, logical position).
+// Peer masks come from a per-warp shared array: every lane atomicOr's its
+// bit into the slot of its digit, reads the slot back and clears it
+// (~5-8 SM cycles per warp op vs ~21 for 7 ballots and ~53 for MATCH.ANY).
 template <int ITEMS>
 __device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* out,
-                                           uint32_t* red) {
+                                           uint32_t* red, uint32_t* pm) {
   const int w = warp_id(), lane = lane_id();
   const uint32_t lt = lanemask_lt();
   uint32_t* mine = dh + w * kRadixBins;
+  uint32_t* mask = pm + w * kRadixBins;
   for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) dh[i] = 0;
   __syncthreads();
   uint32_t rk[ITEMS];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
-    const uint32_t peers = ballot_peers_t<kRadixBits>(d, 0xffffffffu);
+    atomicOr(&mask[d], 1u << lane);
+    __syncwarp();
+    const uint32_t peers = mask[d];
     const uint32_t base = mine[d];
     __syncwarp();
-    if (lane == 31 - __clz(peers)) mine[d] = base + __popc(peers);
+    if (lane == 31 - __clz(peers)) {
+      mine[d] = base + __popc(peers);
+      mask[d] = 0;
+    }
     rk[k] = base + __popc(peers & lt);
     __syncwarp();
   }
@@ -335,6 +340,8 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__
   uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += up16(static_cast<size_t>(stride) * 8);
   uint32_t* toff = reinterpret_cast<uint32_t*>(p); p += up16(static_cast<size_t>(stride) * 4);
   uint32_t* dh = reinterpret_cast<uint32_t*>(p);
+  uint32_t* pm = dh + kDistWarps * kRadixBins;
+  for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) pm[i] = 0;
 
   const int w = warp_id(), lane = lane_id();
 
@@ -409,10 +416,10 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__
       }
       e[k] = (b << kIdxBits) | i;
     }
-    radix_pass<ITEMS>(e, kIdxBits, dh, srtA, red);
+    radix_pass<ITEMS>(e, kIdxBits, dh, srtA, red, pm);
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
-    radix_pass<ITEMS>(e, kIdxBits + kRadixBits, dh, srtB, red);
+    radix_pass<ITEMS>(e, kIdxBits + kRadixBits, dh, srtB, red, pm);
 
     // run starts -> per-bucket tile offsets
 #pragma unroll
