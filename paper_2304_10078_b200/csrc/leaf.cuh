@@ -225,12 +225,17 @@ constexpr int kLeafWarpWarps = 8;
 
 template <typename K>
 struct WarpLeafSmem {
-  K keys[kLeafWarpMax];
+  // key copies while inserting; afterwards the same words are the rank
+  // pass's 32-bit peer masks (cap <= kLeafWarpCap words)
+  alignas(8) unsigned char key_area[kLeafWarpCap * 4 > kLeafWarpMax * sizeof(K) ? kLeafWarpCap * 4
+                                                                                 : kLeafWarpMax * sizeof(K)];
   uint32_t T[kLeafWarpCap];
   uint32_t cell[kLeafWarpCap];
-  uint32_t gstart[kLeafWarpCap];   // also the peer-mask scratch of the rank pass
   uint16_t home[kLeafWarpCap];
   uint16_t gcnt[kLeafWarpCap];
+  uint16_t gstart[kLeafWarpCap];
+  __device__ __forceinline__ K* keys() { return reinterpret_cast<K*>(key_area); }
+  __device__ __forceinline__ uint32_t* masks() { return reinterpret_cast<uint32_t*>(key_area); }
 };
 
 template <typename K, typename V>
@@ -253,7 +258,7 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       if (i < m) {
         key[k] = src_k[lf.lo + i];
         if constexpr (kHasV) val[k] = src_v[lf.lo + i];
-        ws.keys[i] = key[k];
+        ws.keys()[i] = key[k];
       }
     }
     const uint32_t cap = leaf_cap(m), mask = cap - 1;
@@ -261,7 +266,6 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       ws.T[s] = kEmpty32;
       ws.cell[s] = 0;
       ws.gcnt[s] = 0;
-      ws.gstart[s] = 0;
     }
     __syncwarp();
     uint32_t slot[kLeafWarpItems];
@@ -280,26 +284,29 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
           if (prev == kEmpty32) { ws.home[s] = static_cast<uint16_t>(c); break; }
           t = prev;
         }
-        if (ws.keys[t] == key[k]) { atomicMin(&ws.T[s], i); break; }
+        if (ws.keys()[t] == key[k]) { atomicMin(&ws.T[s], i); break; }
         s = (s + 1) & mask;
       }
       slot[k] = s;
     }
     __syncwarp();
     // in-order ranks within groups (records i = lane + 32k, k ascending)
+    uint32_t* pmask = ws.masks();
+    for (uint32_t s = lane; s < cap; s += 32) pmask[s] = 0;
+    __syncwarp();
     uint32_t rank[kLeafWarpItems];
 #pragma unroll
     for (int k = 0; k < kLeafWarpItems; ++k) {
       if (32 * k >= m) { rank[k] = 0; continue; }   // warp-uniform
       const bool valid = lane + 32 * k < m;
-      if (valid) atomicOr(&ws.gstart[slot[k]], 1u << lane);
+      if (valid) atomicOr(&pmask[slot[k]], 1u << lane);
       __syncwarp();
-      const uint32_t peers = valid ? ws.gstart[slot[k]] : 0u;
+      const uint32_t peers = valid ? pmask[slot[k]] : 0u;
       const uint32_t cnt = valid ? ws.gcnt[slot[k]] : 0u;
       __syncwarp();
       if (valid && lane == 31u - __clz(peers)) {
         ws.gcnt[slot[k]] = static_cast<uint16_t>(cnt + __popc(peers));
-        ws.gstart[slot[k]] = 0;
+        pmask[slot[k]] = 0;
       }
       rank[k] = cnt + __popc(peers & lt);
       __syncwarp();

@@ -228,7 +228,8 @@ __global__ void k_write_X(const CT* __restrict__ C, const Node* __restrict__ nod
 // the stable scatter (TMA-pipelined, radix-ranked)
 // ---------------------------------------------------------------------------
 
-constexpr int kDistThreads = 512;
+constexpr int kDistThreads = 256;
+constexpr int kDistCtasPerSm = 2;
 constexpr int kDistWarps = kDistThreads / 32;
 constexpr int kRadixBits = 7;
 constexpr int kRadixBins = 1 << kRadixBits;
@@ -238,7 +239,7 @@ constexpr uint32_t kSentinel = (1u << (2 * kRadixBits)) - 1;   // bucket sorting
 template <typename K, typename V>
 struct DistCfg {
   static constexpr int kValBytes = ValTraits<V>::bytes;
-  static constexpr int kTile = (sizeof(K) + kValBytes) <= 16 ? 4096 : 2048;
+  static constexpr int kTile = (sizeof(K) + kValBytes) <= 16 ? 2048 : 1024;
   static constexpr int kItems = kTile / kDistThreads;
   static constexpr int kPadK = 16 / sizeof(K);
   static constexpr int kPadV = kValBytes ? (16 / kValBytes > 0 ? 16 / kValBytes : 1) : 0;
@@ -314,7 +315,7 @@ __device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift
 }
 
 template <typename K, typename V, typename BF>
-__global__ void __launch_bounds__(kDistThreads, 1)
+__global__ void __launch_bounds__(kDistThreads, kDistCtasPerSm)
 k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__ dk, V* __restrict__ dv,
              const Work* __restrict__ work, uint32_t n_work, const Node* __restrict__ nodes,
              const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below, BF bf) {

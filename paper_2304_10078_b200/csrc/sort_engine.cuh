@@ -38,7 +38,7 @@ inline void launch_distribute(const K* sk, const V* sv, K* dk, V* dv, const Work
   const size_t dsm = dist_smem_bytes_t<K, V>(stride);
   auto kern = k_distribute<K, V, BF>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-  const uint32_t grid = std::min<uint32_t>(nwork, 148);
+  const uint32_t grid = std::min<uint32_t>(nwork, 148 * kDistCtasPerSm);
   kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, bf);
   check_launch();
 }

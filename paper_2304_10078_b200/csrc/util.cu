@@ -383,7 +383,7 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       const size_t dsm = dist_smem_bytes_t<K, V>(pp.stride);
       auto kern = k_distribute<K, V, PartBuckets>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-      kern<<<std::min<uint32_t>(nw, 148), kDistThreads, dsm, st>>>(static_cast<const K*>(keys), static_cast<const V*>(values),
+      kern<<<std::min<uint32_t>(nw, 148 * kDistCtasPerSm), kDistThreads, dsm, st>>>(static_cast<const K*>(keys), static_cast<const V*>(values),
                                           static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
                                           pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf);
     };
