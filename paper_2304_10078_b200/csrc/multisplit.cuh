@@ -228,8 +228,12 @@ __global__ void k_write_X(const CT* __restrict__ C, const Node* __restrict__ nod
 // the stable scatter (TMA-pipelined, radix-ranked)
 // ---------------------------------------------------------------------------
 
-constexpr int kDistThreads = 256;
-constexpr int kDistCtasPerSm = 2;
+constexpr int kDistThreads = 512;
+constexpr int kDistCtasPerSm = 1;
+// Debug / measurement knob (SS_DIST_DEBUG): 0 normal, 1 skip the scattered
+// stores, 2 store linearly (tile-contiguous) -- separates compute cost from
+// the cost of the scatter pattern.  Outputs are wrong unless 0.
+__device__ int g_dist_debug = 0;
 constexpr int kDistWarps = kDistThreads / 32;
 constexpr int kRadixBits = 7;
 constexpr int kRadixBins = 1 << kRadixBits;
@@ -239,7 +243,7 @@ constexpr uint32_t kSentinel = (1u << (2 * kRadixBits)) - 1;   // bucket sorting
 template <typename K, typename V>
 struct DistCfg {
   static constexpr int kValBytes = ValTraits<V>::bytes;
-  static constexpr int kTile = (sizeof(K) + kValBytes) <= 16 ? 2048 : 1024;
+  static constexpr int kTile = (sizeof(K) + kValBytes) <= 16 ? 4096 : 2048;
   static constexpr int kItems = kTile / kDistThreads;
   static constexpr int kPadK = 16 / sizeof(K);
   static constexpr int kPadV = kValBytes ? (16 / kValBytes > 0 ? 16 / kValBytes : 1) : 0;
@@ -343,6 +347,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__
   uint32_t* dh = reinterpret_cast<uint32_t*>(p);
   uint32_t* pm = dh + kDistWarps * kRadixBins;
   for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) pm[i] = 0;
+  const int dbg = g_dist_debug;
 
   const int w = warp_id(), lane = lane_id();
 
@@ -440,9 +445,12 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__
       run_end[k] = false;
       if (b == kSentinel) continue;
       const uint32_t i = ent & ((1u << kIdxBits) - 1);
-      const uint64_t d = cursor[b] + (s - toff[b]);
-      dk[d] = bufK[buf][i + shK];
-      if constexpr (kHasV) dv[d] = bufV[buf][i + shV];
+      uint64_t d = cursor[b] + (s - toff[b]);
+      if (dbg) d = begin + s;
+      if (dbg != 1) {
+        dk[d] = bufK[buf][i + shK];
+        if constexpr (kHasV) dv[d] = bufV[buf][i + shV];
+      }
       run_end[k] = (s + 1 == static_cast<uint32_t>(T)) || ((srtB[s + 1] >> kIdxBits) != b);
     }
     __syncthreads();

@@ -35,6 +35,13 @@ inline void launch_distribute(const K* sk, const V* sv, K* dk, V* dv, const Work
                               const Node* d_nodes, const uint64_t* d_X, uint32_t stride, uint32_t keep_below, BF bf,
                               cudaStream_t st) {
   if (!nwork) return;
+  static const int dbg = [] {
+    const char* e = std::getenv("SS_DIST_DEBUG");
+    const int v = e ? std::atoi(e) : 0;
+    cudaMemcpyToSymbol(g_dist_debug, &v, sizeof(int));
+    return v;
+  }();
+  (void)dbg;
   const size_t dsm = dist_smem_bytes_t<K, V>(stride);
   auto kern = k_distribute<K, V, BF>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
