@@ -30,7 +30,7 @@ template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kCountThreads)
 k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, const Work* __restrict__ work, uint32_t n_work,
             const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, KeyBuckets bf,
-            unsigned long long* __restrict__ HS, uint32_t hs_stride) {
+            unsigned long long* __restrict__ HS, uint32_t hs_stride, uint16_t* __restrict__ ids_out) {
   extern __shared__ __align__(16) uint32_t cnt[];
   __shared__ HeavySmem tab;
   __shared__ unsigned long long hsum[kMaxHeavyDevice];
@@ -62,6 +62,7 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, const Work* __r
         if (valid) {
           const uint32_t b = bf(keys[k], begin + i);
           atomicAdd(&cnt[b], 1u);   // shared atomics are ~free on sm_100 (see count_add)
+          ids_out[begin + i] = static_cast<uint16_t>(b);
           if (SUM && b >= nl)
             atomicAdd(&hsum[b - nl], static_cast<unsigned long long>(val_u64(sv[begin + i])));
         }
@@ -255,6 +256,7 @@ struct AggEngine {
   uint32_t* d_G = nullptr;
   uint64_t* d_loff = nullptr;
   uint64_t* d_part = nullptr;
+  uint16_t* d_ids = nullptr;
   K* d_hk = nullptr;
   uint64_t* d_ha = nullptr;
   uint64_t* d_hoff = nullptr;
@@ -306,6 +308,7 @@ struct AggEngine {
     d_part = a.take<uint64_t>(scan_parts_needed(std::max(max_leaves, max_nodes)) + 8);
     d_hk = a.take<K>(max_nodes * mh);
     d_ha = a.take<uint64_t>(max_nodes * mh);
+    d_ids = a.take<uint16_t>(n);
     d_hoff = a.take<uint64_t>(max_nodes);
   }
 
@@ -420,10 +423,10 @@ struct AggEngine {
     tr.begin(kPhCount);
     if (sum())
       k_count_agg<K, V, true><<<nwork, kCountThreads, stride * 4, st>>>(sk, sv, d_work, nwork, d_nodes, d_C, stride, bf,
-                                                                        d_HS, mh);
+                                                                        d_HS, mh, d_ids);
     else
       k_count_agg<K, V, false><<<nwork, kCountThreads, stride * 4, st>>>(sk, sv, d_work, nwork, d_nodes, d_C, stride,
-                                                                         bf, d_HS, mh);
+                                                                         bf, d_HS, mh, d_ids);
     check_launch();
     tr.launched();
 
@@ -437,7 +440,8 @@ struct AggEngine {
     tr.launched(6);
 
     tr.begin(kPhDistribute);
-    launch_distribute<K, V, KeyBuckets>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets, bf, st);
+    launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets,
+                            P.light_buckets, 0, st);
     tr.launched();
 
     tr.begin(kPhCopy);

@@ -86,6 +86,7 @@ struct PhasePlan {
   uint64_t* d_samp;
   uint64_t leaf_words_n;
   uint64_t s_cap;
+  uint16_t* d_ids;
 
   void carve(Arena& a, uint64_t n, uint32_t stride_, const Params& P, int key_bytes) {
     stride = (stride_ + 1) & ~1u;
@@ -104,6 +105,7 @@ struct PhasePlan {
     d_leafscr = a.take<uint32_t>(leaf_words_n);
     s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
     d_samp = a.take<uint64_t>(2 * s_cap + 2 * pow2_ge(s_cap));
+    d_ids = a.take<uint16_t>(n);
   }
 
   // One node spanning [0, n), rows of exactly subarray_len records.
@@ -476,7 +478,7 @@ int ss_count_matrix(const void* keys, const void* ids, uint64_t n, uint32_t key_
       if (ids) {
         IdBuckets bf{static_cast<const int32_t*>(ids), n_buckets};
         k_count<K, IdBuckets><<<nw, kCountThreads, pp.stride * 4, st>>>(static_cast<const K*>(keys), pp.d_work, nw,
-                                                                       pp.d_node, pp.d_C, pp.stride, bf);
+                                                                       pp.d_node, pp.d_C, pp.stride, bf, nullptr);
       } else {
         KeyBuckets bf{};
         bf.heavy = pp.d_heavy;
@@ -485,7 +487,7 @@ int ss_count_matrix(const void* keys, const void* ids, uint64_t n, uint32_t key_
         bf.light_bits = P.light_bits;
         bf.identity = identity;
         k_count<K, KeyBuckets><<<nw, kCountThreads, pp.stride * 4, st>>>(static_cast<const K*>(keys), pp.d_work, nw,
-                                                                        pp.d_node, pp.d_C, pp.stride, bf);
+                                                                        pp.d_node, pp.d_C, pp.stride, bf, nullptr);
       }
       check_launch();
     });
@@ -558,11 +560,12 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
     check_launch();
     const uint32_t nw = static_cast<uint32_t>(work.size());
     dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
+      // bucket ids (u16) by the count kernel, then the stable scatter
+      const K* sk = static_cast<const K*>(src_keys);
       if (ids) {
         IdBuckets bf{static_cast<const int32_t*>(ids), n_buckets};
-        launch_distribute<K, V, IdBuckets>(static_cast<const K*>(src_keys), static_cast<const V*>(src_values),
-                                           static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
-                                           pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf, st);
+        k_count<K, IdBuckets><<<nw, kCountThreads, pp.stride * 4, st>>>(sk, pp.d_work, nw, pp.d_node, pp.d_C,
+                                                                       pp.stride, bf, pp.d_ids);
       } else {
         KeyBuckets bf{};
         bf.heavy = pp.d_heavy;
@@ -570,10 +573,13 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
         bf.n_light = P.light_buckets;
         bf.light_bits = P.light_bits;
         bf.identity = identity;
-        launch_distribute<K, V, KeyBuckets>(static_cast<const K*>(src_keys), static_cast<const V*>(src_values),
-                                            static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
-                                            pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf, st);
+        k_count<K, KeyBuckets><<<nw, kCountThreads, pp.stride * 4, st>>>(sk, pp.d_work, nw, pp.d_node, pp.d_C,
+                                                                        pp.stride, bf, pp.d_ids);
       }
+      check_launch();
+      launch_distribute<K, V>(sk, static_cast<const V*>(src_values), pp.d_ids, static_cast<K*>(dst_keys),
+                              static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu,
+                              P.light_buckets, n_buckets, st);
     });
     SS_CUDA(cudaStreamSynchronize(st));
   });

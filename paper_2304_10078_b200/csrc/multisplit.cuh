@@ -11,22 +11,12 @@
 // * scan        three small kernels: partial column sums per row group,
 //               per-node bucket-major scan, and the cursor matrix
 //               X[row][b] = out_base + (column-major exclusive prefix).
-// * k_distribute
-//               persistent, one 512-thread CTA per SM.  Each CTA walks its
-//               subarrays in 4096-record tiles; tile t+1 streams into a
-//               second shared buffer by TMA bulk copy (cp.async.bulk +
-//               mbarrier) while tile t is ranked.  Ranking is a stable
-//               two-pass 7-bit LSD radix sort of (bucket, index) in shared
-//               memory (atomicOr peer masks, per-warp digit counts), so the
-//               per-tile cost is O(tile) rather than O(warps x buckets).
-//               Records are then written as contiguous per-bucket runs from
-//               the staged tile at the SMEM cursors of the subarray's X
-//               row.  Stability and race freedom come from the disjoint
-//               cursor ranges, never from atomics deciding order
-//               (SPEC.md:195).
+// * k_distribute (dist.cuh) consumes the u16 bucket ids the count pass
+//               stores, and scatters each subarray stably through its X row.
 #pragma once
 
 #include "common.cuh"
+#include "dist.cuh"
 #include "tma.cuh"
 #include "types.cuh"
 
@@ -93,7 +83,8 @@ __device__ __forceinline__ void count_add(uint32_t* cnt, uint32_t b, bool valid,
 template <typename K, typename BF>
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_work,
-        const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, BF bf) {
+        const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, BF bf,
+        uint16_t* __restrict__ ids_out) {
   extern __shared__ __align__(16) uint32_t cnt[];
   __shared__ HeavySmem tab;
   for (uint32_t wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
@@ -120,6 +111,7 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
         const bool valid = i < len;
         const uint32_t b = valid ? bf(keys[k], begin + i) : 0u;
         count_add(cnt, b, valid, hot, hot_bits);
+        if (ids_out && valid) ids_out[begin + i] = static_cast<uint16_t>(b);   // consumed by k_distribute
       }
     }
     __syncthreads();
@@ -221,249 +213,6 @@ __global__ void k_write_X(const CT* __restrict__ C, const Node* __restrict__ nod
         run += C[r * stride + b];
       }
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// the stable scatter (TMA-pipelined, radix-ranked)
-// ---------------------------------------------------------------------------
-
-constexpr int kDistThreads = 512;
-constexpr int kDistCtasPerSm = 1;
-// Debug / measurement knob (SS_DIST_DEBUG): 0 normal, 1 skip the scattered
-// stores, 2 store linearly (tile-contiguous) -- separates compute cost from
-// the cost of the scatter pattern.  Outputs are wrong unless 0.
-__device__ int g_dist_debug = 0;
-constexpr int kDistWarps = kDistThreads / 32;
-constexpr int kRadixBits = 7;
-constexpr int kRadixBins = 1 << kRadixBits;
-constexpr uint32_t kIdxBits = 12;                 // tile index bits (tile <= 4096)
-constexpr uint32_t kSentinel = (1u << (2 * kRadixBits)) - 1;   // bucket sorting last
-
-template <typename K, typename V>
-struct DistCfg {
-  static constexpr int kValBytes = ValTraits<V>::bytes;
-  static constexpr int kTile = (sizeof(K) + kValBytes) <= 16 ? 4096 : 2048;
-  static constexpr int kItems = kTile / kDistThreads;
-  static constexpr int kPadK = 16 / sizeof(K);
-  static constexpr int kPadV = kValBytes ? (16 / kValBytes > 0 ? 16 / kValBytes : 1) : 0;
-  static constexpr size_t kBufK = (static_cast<size_t>(kTile) + kPadK) * sizeof(K);
-  static constexpr size_t kBufV = kValBytes ? (static_cast<size_t>(kTile) + kPadV) * kValBytes : 0;
-  static size_t smem_bytes(uint32_t stride) {
-    auto up16 = [](size_t x) { return (x + 15) & ~size_t(15); };
-    return 2 * up16(kBufK) + 2 * up16(kBufV) + 2 * kTile * 4 + up16(static_cast<size_t>(stride) * 8) +
-           up16(static_cast<size_t>(stride) * 4) + 2 * kDistWarps * kRadixBins * 4 + 64;
-  }
-};
-
-template <typename K, typename V>
-__host__ inline size_t dist_smem_bytes_t(uint32_t stride) { return DistCfg<K, V>::smem_bytes(stride); }
-
-// One stable LSD pass over the tile: entries e[k] sit at logical positions
-// w*(32*ITEMS) + k*32 + lane; digit = (e >> shift) & 127.  Writes the
-// entries to `out` ordered by (digit, logical position).
-// Peer masks come from a per-warp shared array: every lane atomicOr's its
-// bit into the slot of its digit, reads the slot back and clears it
-// (~5-8 SM cycles per warp op vs ~21 for 7 ballots and ~53 for MATCH.ANY).
-template <int ITEMS>
-__device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* out,
-                                           uint32_t* red, uint32_t* pm) {
-  const int w = warp_id(), lane = lane_id();
-  const uint32_t lt = lanemask_lt();
-  uint32_t* mine = dh + w * kRadixBins;
-  uint32_t* mask = pm + w * kRadixBins;
-  for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) dh[i] = 0;
-  __syncthreads();
-  uint32_t rk[ITEMS];
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
-    atomicOr(&mask[d], 1u << lane);
-    __syncwarp();
-    const uint32_t peers = mask[d];
-    const uint32_t base = mine[d];
-    __syncwarp();
-    if (lane == 31 - __clz(peers)) {
-      mine[d] = base + __popc(peers);
-      mask[d] = 0;
-    }
-    rk[k] = base + __popc(peers & lt);
-    __syncwarp();
-  }
-  __syncthreads();
-  // exclusive scan in (digit, warp) order: 4 consecutive entries per thread
-  constexpr int kEntries = kDistWarps * kRadixBins;
-  constexpr int kPer = kEntries / kDistThreads;
-  uint32_t v[kPer], s = 0;
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int j = threadIdx.x * kPer + q;          // j = d * kDistWarps + w
-    v[q] = dh[(j % kDistWarps) * kRadixBins + j / kDistWarps];
-    s += v[q];
-  }
-  uint32_t tot;
-  uint32_t run = block_excl_scan<uint32_t>(s, red, tot);
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int j = threadIdx.x * kPer + q;
-    dh[(j % kDistWarps) * kRadixBins + j / kDistWarps] = run;
-    run += v[q];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
-    out[mine[d] + rk[k]] = e[k];
-  }
-  __syncthreads();
-}
-
-template <typename K, typename V, typename BF>
-__global__ void __launch_bounds__(kDistThreads, kDistCtasPerSm)
-k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__ dk, V* __restrict__ dv,
-             const Work* __restrict__ work, uint32_t n_work, const Node* __restrict__ nodes,
-             const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below, BF bf) {
-  using Cfg = DistCfg<K, V>;
-  constexpr bool kHasV = Cfg::kValBytes > 0;
-  constexpr int T = Cfg::kTile;
-  constexpr int ITEMS = Cfg::kItems;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ HeavySmem tab;
-  __shared__ uint32_t red[33];
-  __shared__ __align__(8) uint64_t bars[2];
-
-  auto up16 = [](size_t x) { return (x + 15) & ~size_t(15); };
-  unsigned char* p = smem;
-  K* bufK[2];
-  V* bufV[2];
-  bufK[0] = reinterpret_cast<K*>(p); p += up16(Cfg::kBufK);
-  bufK[1] = reinterpret_cast<K*>(p); p += up16(Cfg::kBufK);
-  bufV[0] = reinterpret_cast<V*>(p); p += up16(Cfg::kBufV);
-  bufV[1] = reinterpret_cast<V*>(p); p += up16(Cfg::kBufV);
-  uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
-  uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
-  uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += up16(static_cast<size_t>(stride) * 8);
-  uint32_t* toff = reinterpret_cast<uint32_t*>(p); p += up16(static_cast<size_t>(stride) * 4);
-  uint32_t* dh = reinterpret_cast<uint32_t*>(p);
-  uint32_t* pm = dh + kDistWarps * kRadixBins;
-  for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) pm[i] = 0;
-  const int dbg = g_dist_debug;
-
-  const int w = warp_id(), lane = lane_id();
-
-  // tile iterator over this CTA's work items
-  struct It {
-    uint32_t wi;
-    uint32_t tb;
-  };
-  auto first_it = [&](uint32_t wi0) {
-    It it{wi0, 0};
-    while (it.wi < n_work && work[it.wi].len == 0) it.wi += gridDim.x;
-    return it;
-  };
-  auto next_it = [&](It it) {
-    it.tb += T;
-    if (it.tb >= work[it.wi].len) it = first_it(it.wi + gridDim.x);
-    return it;
-  };
-  auto issue = [&](It it, int buf) {   // one thread
-    const Work wk = work[it.wi];
-    const uint64_t begin = wk.begin + it.tb;
-    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - it.tb);
-    uint32_t bytes = span_body_bytes(sk, begin, cnt);
-    if constexpr (kHasV) bytes += span_body_bytes(sv, begin, cnt);
-    fence_proxy_async();
-    mbar_arrive_expect_tx(&bars[buf], bytes);
-    stage_span(bufK[buf], sk, begin, cnt, &bars[buf]);
-    if constexpr (kHasV) stage_span(bufV[buf], sv, begin, cnt, &bars[buf]);
-  };
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  It cur = first_it(blockIdx.x);
-  if (cur.wi >= n_work) return;
-  if (threadIdx.x == 0) issue(cur, 0);
-  uint32_t q = 0;
-  uint32_t nb = 0;
-  while (cur.wi < n_work) {
-    const int buf = q & 1;
-    const It nxt = next_it(cur);
-    if (threadIdx.x == 0 && nxt.wi < n_work) issue(nxt, buf ^ 1);
-    const Work wk = work[cur.wi];
-    if (cur.tb == 0) {   // new subarray: its node's table and X row
-      const Node nd = nodes[wk.node];
-      bf.prepare(nd, wk.node, &tab);
-      nb = min(bf.n_buckets(), keep_below);
-      const uint64_t* xrow = X + wk.row * stride;
-      for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) cursor[b] = xrow[b];
-    }
-    const uint64_t begin = wk.begin + cur.tb;
-    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - cur.tb);
-    const uint32_t shK = Span16<K>(sk, begin, cnt).sh;
-    uint32_t shV = 0;
-    if constexpr (kHasV) shV = Span16<V>(sv, begin, cnt).sh;
-    mbar_wait(&bars[buf], (q >> 1) & 1);
-    __syncthreads();   // head/tail elements, cursors and the table are visible
-
-    // bucket of every record -> (bucket << 12) | tile index
-    uint32_t e[ITEMS];
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
-      uint32_t b = kSentinel;
-      if (i < cnt) {
-        b = bf(bufK[buf][i + shK], begin + i);
-        if (b >= nb) b = kSentinel;
-      }
-      e[k] = (b << kIdxBits) | i;
-    }
-    radix_pass<ITEMS>(e, kIdxBits, dh, srtA, red, pm);
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
-    radix_pass<ITEMS>(e, kIdxBits + kRadixBits, dh, srtB, red, pm);
-
-    // run starts -> per-bucket tile offsets
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t s = threadIdx.x + k * kDistThreads;
-      const uint32_t b = srtB[s] >> kIdxBits;
-      if (b != kSentinel && (s == 0 || (srtB[s - 1] >> kIdxBits) != b)) toff[b] = s;
-    }
-    __syncthreads();
-    // contiguous per-bucket runs out of the staged tile
-    bool run_end[ITEMS];
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t s = threadIdx.x + k * kDistThreads;
-      const uint32_t ent = srtB[s];
-      const uint32_t b = ent >> kIdxBits;
-      run_end[k] = false;
-      if (b == kSentinel) continue;
-      const uint32_t i = ent & ((1u << kIdxBits) - 1);
-      uint64_t d = cursor[b] + (s - toff[b]);
-      if (dbg) d = begin + s;
-      if (dbg != 1) {
-        dk[d] = bufK[buf][i + shK];
-        if constexpr (kHasV) dv[d] = bufV[buf][i + shV];
-      }
-      run_end[k] = (s + 1 == static_cast<uint32_t>(T)) || ((srtB[s + 1] >> kIdxBits) != b);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      if (!run_end[k]) continue;
-      const uint32_t s = threadIdx.x + k * kDistThreads;
-      const uint32_t b = srtB[s] >> kIdxBits;
-      cursor[b] += s + 1 - toff[b];
-    }
-    __syncthreads();   // buffer `buf` may be refilled; cursors final for the next tile
-    cur = nxt;
-    ++q;
   }
 }
 

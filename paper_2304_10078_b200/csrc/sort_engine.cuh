@@ -30,10 +30,25 @@ inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
   return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
 }
 
-template <typename K, typename V, typename BF>
-inline void launch_distribute(const K* sk, const V* sv, K* dk, V* dv, const Work* d_work, uint32_t nwork,
-                              const Node* d_nodes, const uint64_t* d_X, uint32_t stride, uint32_t keep_below, BF bf,
-                              cudaStream_t st) {
+template <typename K, typename V, int TILE>
+inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
+                                uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
+                                uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st) {
+  const size_t dsm = DistCfg<K, V, TILE>::smem_bytes(stride);
+  auto kern = k_distribute<K, V, TILE>;
+  SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
+  const uint32_t grid = std::min<uint32_t>(nwork, 148 * kDistCtasPerSm);
+  kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
+                                        n_light, fixed_nb);
+  check_launch();
+}
+
+// Stable scatter of every work item through its X row, by the u16 bucket
+// ids `ids` the count pass stored.
+template <typename K, typename V>
+inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
+                              uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
+                              uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st) {
   if (!nwork) return;
   static const int dbg = [] {
     const char* e = std::getenv("SS_DIST_DEBUG");
@@ -42,12 +57,20 @@ inline void launch_distribute(const K* sk, const V* sv, K* dk, V* dv, const Work
     return v;
   }();
   (void)dbg;
-  const size_t dsm = dist_smem_bytes_t<K, V>(stride);
-  auto kern = k_distribute<K, V, BF>;
-  SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-  const uint32_t grid = std::min<uint32_t>(nwork, 148 * kDistCtasPerSm);
-  kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, bf);
-  check_launch();
+  if (stride >= kMaxDistBuckets) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
+  switch (dist_tile_for<K, V>(stride)) {
+    case 4096:
+      launch_distribute_t<K, V, 4096>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
+                                      fixed_nb, st);
+      break;
+    case 2048:
+      launch_distribute_t<K, V, 2048>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
+                                      fixed_nb, st);
+      break;
+    default:
+      launch_distribute_t<K, V, 1024>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
+                                      fixed_nb, st);
+  }
 }
 
 template <typename K, typename V>
@@ -85,6 +108,7 @@ struct SortEngine {
   Leaf* d_leaf_g = nullptr;   // global-scratch CTA leaves
   uint64_t* d_samp = nullptr;
   uint32_t* d_leafscr = nullptr;
+  uint16_t* d_ids = nullptr;   // per-record bucket ids of the current level
   bool external_scratch = false;
 
   void plan(Arena& a, bool carve_scratch = true) {
@@ -119,6 +143,7 @@ struct SortEngine {
     d_leaf_g = a.take<Leaf>(max_leaves);
     d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * (2 * s_cap + 2 * pow2_ge(s_cap)));
     d_leafscr = a.take<uint32_t>(static_cast<uint64_t>(leafg_grid) * leafg_words);
+    d_ids = a.take<uint16_t>(n);
   }
 
   bool src_is_A(int level, bool flip) const { return ((level & 1) == 1) != flip; }
@@ -270,7 +295,8 @@ struct SortEngine {
 
     // counting matrix
     tr.begin(kPhCount);
-    k_count<K, KeyBuckets><<<nwork, kCountThreads, stride * 4, st>>>(sk, d_work, nwork, d_nodes, d_C, stride, bf);
+    k_count<K, KeyBuckets><<<nwork, kCountThreads, stride * 4, st>>>(sk, d_work, nwork, d_nodes, d_C, stride, bf,
+                                                                     d_ids);
     check_launch();
     tr.launched();
 
@@ -287,7 +313,8 @@ struct SortEngine {
 
     // blocked distributing
     tr.begin(kPhDistribute);
-    launch_distribute<K, V, KeyBuckets>(sk, sv, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu, bf, st);
+    launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu,
+                            P.light_buckets, 0, st);
     check_launch();
     tr.launched();
 

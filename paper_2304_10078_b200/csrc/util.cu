@@ -207,6 +207,7 @@ struct PartPlan {
   uint64_t* d_X;
   uint64_t* d_P;
   uint64_t* d_off;
+  uint16_t* d_ids;
   void carve(Arena& a, uint64_t n, uint32_t parts) {
     stride = (parts + 1) & ~1u;
     rows = std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(n, 4096)));
@@ -218,6 +219,7 @@ struct PartPlan {
     d_X = a.take<uint64_t>(rows * stride);
     d_P = a.take<uint64_t>(grps * stride);
     d_off = a.take<uint64_t>(stride + 1);
+    d_ids = a.take<uint16_t>(n);
   }
 };
 
@@ -374,18 +376,19 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       using K = decltype(kt);
       using V = decltype(vt);
       k_count<K, PartBuckets><<<nw, kCountThreads, pp.stride * 4, st>>>(static_cast<const K*>(keys), pp.d_work, nw,
-                                                                      pp.d_node, pp.d_C, pp.stride, bf);
+                                                                      pp.d_node, pp.d_C, pp.stride, bf, pp.d_ids);
       k_colsum_groups<uint32_t><<<nd.n_grps, 256, 0, st>>>(pp.d_C, pp.d_node, pp.d_gn, nd.n_grps, pp.d_P, pp.stride, 0, 0,
                                                            parts);
       k_scan_nodes<<<1, 1024, 0, st>>>(pp.d_node, 1, pp.d_P, pp.d_off, pp.stride, 0, 0, parts, nullptr);
       k_write_X<uint32_t, uint64_t><<<nd.n_grps, 256, 0, st>>>(pp.d_C, pp.d_node, pp.d_gn, nd.n_grps, pp.d_P, pp.d_X,
                                                                 pp.stride, 0, 0, parts, nullptr);
-      const size_t dsm = dist_smem_bytes_t<K, V>(pp.stride);
-      auto kern = k_distribute<K, V, PartBuckets>;
+      constexpr int kTile = 2048;   // parts <= 4096 always fit this tile
+      const size_t dsm = DistCfg<K, V, kTile>::smem_bytes(pp.stride);
+      auto kern = k_distribute<K, V, kTile>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-      kern<<<std::min<uint32_t>(nw, 148 * kDistCtasPerSm), kDistThreads, dsm, st>>>(static_cast<const K*>(keys), static_cast<const V*>(values),
-                                          static_cast<K*>(dst_keys), static_cast<V*>(dst_values), pp.d_work, nw,
-                                          pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, bf);
+      kern<<<std::min<uint32_t>(nw, 148 * kDistCtasPerSm), kDistThreads, dsm, st>>>(
+          static_cast<const K*>(keys), static_cast<const V*>(values), pp.d_ids, static_cast<K*>(dst_keys),
+          static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, 0, parts);
     };
     auto withv = [&](auto kt) {
       using K = decltype(kt);
