@@ -49,12 +49,13 @@ struct DistCfg {
   static constexpr size_t kBufK = up16((static_cast<size_t>(kTile) + 16 / sizeof(K)) * sizeof(K));
   static constexpr size_t kBufV = kValBytes ? up16((static_cast<size_t>(kTile) + 16) * kValBytes) : 0;
   static size_t smem_bytes(uint32_t stride) {
-    return 2 * (kBufI + kBufK + kBufV) + 2 * static_cast<size_t>(kTile) * 4 + up16(static_cast<size_t>(stride) * 8) +
-           2 * up16(static_cast<size_t>(stride) * 4) + 2 * kDistWarps * kRadixBins * 4 + 64;
+    return 2 * (kBufI + kBufK + kBufV) + 2 * static_cast<size_t>(kTile) * 4 +
+           2 * up16(static_cast<size_t>(stride) * 8) + up16(static_cast<size_t>(stride) * 4) +
+           2 * kDistWarps * kRadixBins * 4 + 64;
   }
 };
 
-constexpr size_t kMaxDynSmem = 227 * 1024;
+constexpr size_t kMaxDynSmem = 227 * 1024 - 1024;   // leave room for static shared memory
 
 // Largest tile (4096, 2048 or 1024 records) whose buffers fit shared memory.
 template <typename K, typename V>
@@ -64,19 +65,19 @@ __host__ inline int dist_tile_for(uint32_t stride) {
   return 1024;
 }
 
-// One stable LSD pass over the tile: entries e[k] sit at logical positions
-// w*(32*ITEMS) + k*32 + lane; digit = (e >> shift) & 127.  Writes the
-// entries to `out` ordered by (digit, logical position).
+// Per-warp stable ranks of one LSD digit: e[k] at logical position
+// w*(32*ITEMS) + k*32 + lane, digit = (e >> shift) & 127.  Leaves the warp's
+// digit counts in dh[w][*] and each item's rank among equal digits of its
+// warp (index order) in rk[k].
 template <int ITEMS>
-__device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* out,
-                                           uint32_t* red, uint32_t* pm) {
+__device__ __forceinline__ void radix_rank(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* pm,
+                                           uint32_t (&rk)[ITEMS]) {
   const int w = warp_id(), lane = lane_id();
   const uint32_t lt = lanemask_lt();
   uint32_t* mine = dh + w * kRadixBins;
   uint32_t* mask = pm + w * kRadixBins;
   for (int i = lane; i < kRadixBins; i += 32) mine[i] = 0;
   __syncwarp();
-  uint32_t rk[ITEMS];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
@@ -92,8 +93,12 @@ __device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift
     rk[k] = base + __popc(peers & lt);
     __syncwarp();
   }
-  __syncthreads();
-  // exclusive scan in (digit, warp) order: kPer consecutive entries per thread
+}
+
+// (digit, warp)-major exclusive scan of dh in place: kPer entries per
+// thread.  `extra` (< 2^32 in total) is scanned alongside in the high half.
+__device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, uint32_t* red32, unsigned long long* red64,
+                                               uint32_t extra) {
   constexpr int kEntries = kDistWarps * kRadixBins;
   constexpr int kPer = kEntries / kDistThreads;
   uint32_t v[kPer], s = 0;
@@ -103,15 +108,24 @@ __device__ __forceinline__ void radix_pass(const uint32_t (&e)[ITEMS], int shift
     v[q] = dh[(j % kDistWarps) * kRadixBins + j / kDistWarps];
     s += v[q];
   }
-  uint32_t tot;
-  uint32_t run = block_excl_scan<uint32_t>(s, red, tot);
+  unsigned long long tot;
+  const unsigned long long packed = (static_cast<unsigned long long>(extra) << 32) | s;
+  const unsigned long long ex = block_excl_scan<unsigned long long>(packed, red64, tot);
+  uint32_t run = static_cast<uint32_t>(ex);
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x * kPer + q;
     dh[(j % kDistWarps) * kRadixBins + j / kDistWarps] = run;
     run += v[q];
   }
-  __syncthreads();
+  (void)red32;
+  return static_cast<uint32_t>(ex >> 32);
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void radix_scatter(const uint32_t (&e)[ITEMS], const uint32_t (&rk)[ITEMS], int shift,
+                                              const uint32_t* dh, uint32_t* out) {
+  const uint32_t* mine = dh + warp_id() * kRadixBins;
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
@@ -134,6 +148,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   constexpr int ITEMS = Cfg::kItems;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t red[33];
+  __shared__ unsigned long long red64[33];
   __shared__ __align__(8) uint64_t bars[2];
 
   unsigned char* p = smem;
@@ -148,32 +163,22 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
   uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
   uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
+  // hist (u32) during ranking, then the tile's write base cursor-toff (u64)
+  uint64_t* wbase = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
   uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
-  uint32_t* toff = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
   uint32_t* dh = reinterpret_cast<uint32_t*>(p);
   uint32_t* pm = dh + kDistWarps * kRadixBins;
   for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) pm[i] = 0;
   const int dbg = g_dist_debug;
   const int w = warp_id(), lane = lane_id();
 
-  struct It {
-    uint32_t wi;
-    uint32_t tb;
+  auto next_valid = [&](uint32_t i) {
+    while (i < n_work && work[i].len == 0) i += gridDim.x;
+    return i;
   };
-  auto first_it = [&](uint32_t wi0) {
-    It it{wi0, 0};
-    while (it.wi < n_work && work[it.wi].len == 0) it.wi += gridDim.x;
-    return it;
-  };
-  auto next_it = [&](It it) {
-    it.tb += T;
-    if (it.tb >= work[it.wi].len) it = first_it(it.wi + gridDim.x);
-    return it;
-  };
-  auto issue = [&](It it, int b) {   // one thread
-    const Work wk = work[it.wi];
-    const uint64_t begin = wk.begin + it.tb;
-    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - it.tb);
+  auto issue = [&](const Work& wk, uint32_t tb, int b) {   // one thread
+    const uint64_t begin = wk.begin + tb;
+    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - tb);
     uint32_t bytes = span_body_bytes(ids, begin, cnt) + span_body_bytes(sk, begin, cnt);
     if constexpr (kHasV) bytes += span_body_bytes(sv, begin, cnt);
     fence_proxy_async();
@@ -188,26 +193,46 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     mbar_init(&bars[1], 1);
     fence_barrier_init();
   }
-  __syncthreads();
-
-  It cur = first_it(blockIdx.x);
-  if (cur.wi >= n_work) return;
-  if (threadIdx.x == 0) issue(cur, 0);
-  uint32_t q = 0, nb = 0;
-  while (cur.wi < n_work) {
-    const int buf = q & 1;
-    const It nxt = next_it(cur);
-    if (threadIdx.x == 0 && nxt.wi < n_work) issue(nxt, buf ^ 1);
-    const Work wk = work[cur.wi];
-    if (cur.tb == 0) {   // new subarray: its X row and bucket count
-      nb = fixed_nb ? fixed_nb : n_light + nodes[wk.node].n_heavy;
-      if (nb > keep_below) nb = keep_below;
-      const uint64_t* xrow = X + wk.row * stride;
-      for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) cursor[b] = xrow[b];
+  // consumer state: current work item, cached in registers
+  uint32_t wi = next_valid(blockIdx.x);
+  if (wi >= n_work) return;
+  Work cw = work[wi];
+  uint32_t tb = 0;
+  // producer state (thread 0 only): next tile to stage
+  uint32_t pwi = wi, ptb = 0;
+  Work pw = cw;
+  auto padvance = [&]() {
+    ptb += T;
+    if (ptb >= pw.len) {
+      pwi = next_valid(pwi + gridDim.x);
+      ptb = 0;
+      if (pwi < n_work) pw = work[pwi];
     }
-    for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) hist[b] = 0;
-    const uint64_t begin = wk.begin + cur.tb;
-    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - cur.tb);
+  };
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    issue(pw, ptb, 0);
+    padvance();
+  }
+  uint32_t nb = 0;
+  bool fresh = true;
+  for (uint32_t q = 0;; ++q) {
+    const int buf = q & 1;
+    if (threadIdx.x == 0 && pwi < n_work) {
+      issue(pw, ptb, buf ^ 1);
+      padvance();
+    }
+    if (fresh) {   // new subarray: its X row and bucket count
+      nb = fixed_nb ? fixed_nb : n_light + nodes[cw.node].n_heavy;
+      if (nb > keep_below) nb = keep_below;
+      const uint64_t* xrow = X + cw.row * stride;
+      for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) {
+        cursor[b] = xrow[b];
+        hist[b] = 0;
+      }
+    }
+    const uint64_t begin = cw.begin + tb;
+    const uint32_t cnt = min(static_cast<uint32_t>(T), cw.len - tb);
     const uint32_t shI = Span16<uint16_t>(ids, begin, cnt).sh;
     const uint32_t shK = Span16<K>(sk, begin, cnt).sh;
     uint32_t shV = 0;
@@ -215,8 +240,8 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     mbar_wait(&bars[buf], (q >> 1) & 1);
     __syncthreads();   // head/tail elements, cursors, zeroed histogram visible
 
-    // ids of the tile -> histogram + (bucket << 12 | index) entries
-    uint32_t e[ITEMS];
+    // ids -> histogram + (bucket << 12 | index) entries; pass-1 ranks
+    uint32_t e[ITEMS], rk[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
       const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
@@ -228,23 +253,31 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       }
       e[k] = (b << kIdxBits) | i;
     }
-    radix_pass<ITEMS>(e, kIdxBits, dh, srtA, red, pm);
-    // bucket starts inside the sorted tile (scan of the histogram)
-    {
-      const uint32_t per = (nb + kDistThreads - 1) / kDistThreads;
-      const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
-      uint32_t local = 0;
-      for (uint32_t b = b0; b < b1; ++b) local += hist[b];
-      uint32_t tot;
-      uint32_t run = block_excl_scan<uint32_t>(local, red, tot);   // also fences the pass-1 scatter
-      for (uint32_t b = b0; b < b1; ++b) {
-        toff[b] = run;
-        run += hist[b];
-      }
+    radix_rank<ITEMS>(e, kIdxBits, dh, pm, rk);
+    __syncthreads();
+    // one fused scan: pass-1 digit bases and the histogram (bucket starts)
+    const uint32_t per = (nb + kDistThreads - 1) / kDistThreads;
+    const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
+    uint32_t hl = 0;
+    for (uint32_t b = b0; b < b1; ++b) hl += hist[b];
+    uint32_t trun = radix_scan(dh, red, red64, hl);
+    for (uint32_t b = b0; b < b1; ++b) {   // thread-owned buckets: no races
+      const uint32_t h = hist[b];
+      wbase[b] = cursor[b] - trun;
+      cursor[b] += h;
+      hist[b] = 0;
+      trun += h;
     }
+    __syncthreads();
+    radix_scatter<ITEMS>(e, rk, kIdxBits, dh, srtA);
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
-    radix_pass<ITEMS>(e, kIdxBits + kRadixBits, dh, srtB, red, pm);
+    radix_rank<ITEMS>(e, kIdxBits + kRadixBits, dh, pm, rk);
+    __syncthreads();
+    radix_scan(dh, red, red64, 0);
+    __syncthreads();
+    radix_scatter<ITEMS>(e, rk, kIdxBits + kRadixBits, dh, srtB);
     __syncthreads();
     // contiguous per-bucket runs out of the staged tile
 #pragma unroll
@@ -254,18 +287,23 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       const uint32_t b = ent >> kIdxBits;
       if (b == kSentinel) continue;
       const uint32_t i = ent & ((1u << kIdxBits) - 1);
-      uint64_t d = cursor[b] + (s - toff[b]);
+      uint64_t d = wbase[b] + s;
       if (dbg) d = begin + s;
       if (dbg != 1) {
         dk[d] = bufK[buf][i + shK];
         if constexpr (kHasV) dv[d] = bufV[buf][i + shV];
       }
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) cursor[b] += hist[b];
-    __syncthreads();   // buffer `buf` may be refilled; cursors final for the next tile
-    cur = nxt;
-    ++q;
+    // advance (registers only, unless a new work item starts)
+    tb += T;
+    fresh = tb >= cw.len;
+    if (fresh) {
+      wi = next_valid(wi + gridDim.x);
+      if (wi >= n_work) break;
+      cw = work[wi];
+      tb = 0;
+    }
+    __syncthreads();   // buffer `buf` may be refilled; wbase / srtB reusable
   }
 }
 

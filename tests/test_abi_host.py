@@ -52,7 +52,7 @@ def test_workspace_sizes_scale():
         ws = L.ss_semisort_workspace_bytes(n, 8, 8, ctypes.byref(P))
         assert ws >= 16 * n
         if n == 10**9:
-            assert ws < 24 * n       # scratch + bounded level structures
+            assert ws < 26 * n       # scratch + u16 ids + bounded level structures
         wa = L.ss_aggregate_workspace_bytes(n, 8, 8, ctypes.byref(P))
         assert wa >= 32 * n
 
