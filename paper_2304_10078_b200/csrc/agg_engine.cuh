@@ -441,7 +441,7 @@ struct AggEngine {
 
     tr.begin(kPhDistribute);
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets,
-                            P.light_buckets, 0, st);
+                            P.light_buckets, 0, st, n);
     tr.launched();
 
     tr.begin(kPhCopy);

@@ -579,7 +579,7 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
       check_launch();
       launch_distribute<K, V>(sk, static_cast<const V*>(src_values), pp.d_ids, static_cast<K*>(dst_keys),
                               static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu,
-                              P.light_buckets, n_buckets, st);
+                              P.light_buckets, n_buckets, st, n);
     });
     SS_CUDA(cudaStreamSynchronize(st));
   });

@@ -6,7 +6,8 @@
 // Per tile:
 //   * TMA bulk copies (cp.async.bulk + mbarrier) stream ids, keys and
 //     values of tile t+1 into the second half of a double buffer while
-//     tile t is processed;
+//     tile t is processed (the 16-byte aligned superset of the tile, so the
+//     issuing thread never waits on a global load);
 //   * a shared-atomic histogram of the tile's ids and one block scan give
 //     every bucket's start inside the tile (no run-boundary pass);
 //   * a stable two-pass 7-bit LSD radix sort of (id << 12 | index) in
@@ -14,8 +15,8 @@
 //     a digit inside a warp come from shared atomicOr masks, which cost
 //     ~5-8 SM cycles per warp op on sm_100 against ~53 for MATCH.ANY
 //     (tools/peers_bench.cu);
-//   * records leave as contiguous per-bucket runs at the subarray's SMEM
-//     cursors (its X row), then the cursors advance by the tile histogram.
+//   * records leave as contiguous per-bucket runs at the subarray's
+//     cursors (its X row); the cursors advance by the tile histogram.
 // Stability and race freedom come from disjoint cursor ranges, never from
 // atomics deciding order.
 #pragma once
@@ -45,13 +46,15 @@ struct DistCfg {
   static constexpr int kTile = TILE;
   static constexpr int kItems = kTile / kDistThreads;
   static constexpr size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t kBufI = up16((static_cast<size_t>(kTile) + 8) * 2);
-  static constexpr size_t kBufK = up16((static_cast<size_t>(kTile) + 16 / sizeof(K)) * sizeof(K));
-  static constexpr size_t kBufV = kValBytes ? up16((static_cast<size_t>(kTile) + 16) * kValBytes) : 0;
+  // +2 x (16 / element size) elements: the aligned superset of a tile
+  static constexpr size_t kBufI = up16((static_cast<size_t>(kTile) + 16) * 2);
+  static constexpr size_t kBufK = up16((static_cast<size_t>(kTile) + 2 * (16 / sizeof(K))) * sizeof(K));
+  static constexpr size_t kBufV =
+      kValBytes ? up16((static_cast<size_t>(kTile) + 2 * (16 / kValBytes > 0 ? 16 / kValBytes : 1)) * kValBytes) : 0;
+  static constexpr size_t kSet = kBufI + kBufK + kBufV;   // one pipeline stage
   static size_t smem_bytes(uint32_t stride) {
-    return 2 * (kBufI + kBufK + kBufV) + 2 * static_cast<size_t>(kTile) * 4 +
-           2 * up16(static_cast<size_t>(stride) * 8) + up16(static_cast<size_t>(stride) * 4) +
-           2 * kDistWarps * kRadixBins * 4 + 64;
+    return 2 * kSet + 2 * static_cast<size_t>(kTile) * 4 + 2 * up16(static_cast<size_t>(stride) * 8) +
+           up16(static_cast<size_t>(stride) * 4) + 2 * kDistWarps * kRadixBins * 4 + 64;
   }
 };
 
@@ -97,8 +100,7 @@ __device__ __forceinline__ void radix_rank(const uint32_t (&e)[ITEMS], int shift
 
 // (digit, warp)-major exclusive scan of dh in place: kPer entries per
 // thread.  `extra` (< 2^32 in total) is scanned alongside in the high half.
-__device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, uint32_t* red32, unsigned long long* red64,
-                                               uint32_t extra) {
+__device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, unsigned long long* red64, uint32_t extra) {
   constexpr int kEntries = kDistWarps * kRadixBins;
   constexpr int kPer = kEntries / kDistThreads;
   uint32_t v[kPer], s = 0;
@@ -118,7 +120,6 @@ __device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, uint32_t* red32, un
     dh[(j % kDistWarps) * kRadixBins + j / kDistWarps] = run;
     run += v[q];
   }
-  (void)red32;
   return static_cast<uint32_t>(ex >> 32);
 }
 
@@ -135,10 +136,11 @@ __device__ __forceinline__ void radix_scatter(const uint32_t (&e)[ITEMS], const 
 
 // ids: u16 bucket id per source record (absolute index), written by the
 // count pass.  Buckets kept: [0, nb) with nb = min(fixed_nb or
-// n_light + node.n_heavy, keep_below); others are dropped.
+// n_light + node.n_heavy, keep_below); others are dropped.  n_src: element
+// count of the source arrays (bounds of the aligned TMA supersets).
 template <typename K, typename V, int TILE>
 __global__ void __launch_bounds__(kDistThreads, kDistCtasPerSm)
-k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids,
+k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
              K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
              const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
              uint32_t n_light, uint32_t fixed_nb) {
@@ -147,23 +149,18 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   constexpr int T = Cfg::kTile;
   constexpr int ITEMS = Cfg::kItems;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t red[33];
   __shared__ unsigned long long red64[33];
   __shared__ __align__(8) uint64_t bars[2];
 
-  unsigned char* p = smem;
-  uint16_t* bufI[2];
-  K* bufK[2];
-  V* bufV[2];
-  for (int b = 0; b < 2; ++b) {
-    bufI[b] = reinterpret_cast<uint16_t*>(p); p += Cfg::kBufI;
-    bufK[b] = reinterpret_cast<K*>(p); p += Cfg::kBufK;
-    bufV[b] = reinterpret_cast<V*>(p); p += Cfg::kBufV;
-  }
+  // stage b: [ids | keys | values] at smem + b * kSet (arithmetic keeps the
+  // shared address space visible to the compiler: LDS, no local arrays)
+  auto stI = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * Cfg::kSet); };
+  auto stK = [&](int b) { return reinterpret_cast<K*>(smem + b * Cfg::kSet + Cfg::kBufI); };
+  auto stV = [&](int b) { return reinterpret_cast<V*>(smem + b * Cfg::kSet + Cfg::kBufI + Cfg::kBufK); };
+  unsigned char* p = smem + 2 * Cfg::kSet;
   uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
   uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
   uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
-  // hist (u32) during ranking, then the tile's write base cursor-toff (u64)
   uint64_t* wbase = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
   uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
   uint32_t* dh = reinterpret_cast<uint32_t*>(p);
@@ -176,16 +173,21 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     while (i < n_work && work[i].len == 0) i += gridDim.x;
     return i;
   };
-  auto issue = [&](const Work& wk, uint32_t tb, int b) {   // one thread
+  auto issue = [&](const Work& wk, uint32_t tb, int b) {   // one thread, never blocks
     const uint64_t begin = wk.begin + tb;
     const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - tb);
-    uint32_t bytes = span_body_bytes(ids, begin, cnt) + span_body_bytes(sk, begin, cnt);
-    if constexpr (kHasV) bytes += span_body_bytes(sv, begin, cnt);
+    const Bulk16<uint16_t> bi(ids, n_src, begin, cnt);
+    const Bulk16<K> bk(sk, n_src, begin, cnt);
+    uint32_t bytes = bi.bytes + bk.bytes;
+    Bulk16<V> bv(sv, n_src, begin, cnt);
+    if constexpr (kHasV) bytes += bv.bytes;
     fence_proxy_async();
     mbar_arrive_expect_tx(&bars[b], bytes);
-    stage_span(bufI[b], ids, begin, cnt, &bars[b]);
-    stage_span(bufK[b], sk, begin, cnt, &bars[b]);
-    if constexpr (kHasV) stage_span(bufV[b], sv, begin, cnt, &bars[b]);
+    if (bi.ok) bulk_g2s(stI(b), bi.src, bi.bytes, &bars[b]);
+    if (bk.ok) bulk_g2s(stK(b), bk.src, bk.bytes, &bars[b]);
+    if constexpr (kHasV) {
+      if (bv.ok) bulk_g2s(stV(b), bv.src, bv.bytes, &bars[b]);
+    }
   };
 
   if (threadIdx.x == 0) {
@@ -233,12 +235,14 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     }
     const uint64_t begin = cw.begin + tb;
     const uint32_t cnt = min(static_cast<uint32_t>(T), cw.len - tb);
-    const uint32_t shI = Span16<uint16_t>(ids, begin, cnt).sh;
-    const uint32_t shK = Span16<K>(sk, begin, cnt).sh;
-    uint32_t shV = 0;
-    if constexpr (kHasV) shV = Span16<V>(sv, begin, cnt).sh;
+    const Bulk16<uint16_t> pi(ids, n_src, begin, cnt);
+    const Bulk16<K> pk(sk, n_src, begin, cnt);
+    const Bulk16<V> pv(sv, n_src, begin, cnt);
+    const uint16_t* tI = stI(buf) + pi.sh;
+    const K* tK = stK(buf) + pk.sh;
+    const V* tV = stV(buf) + pv.sh;
     mbar_wait(&bars[buf], (q >> 1) & 1);
-    __syncthreads();   // head/tail elements, cursors, zeroed histogram visible
+    __syncthreads();   // cursors and zeroed histogram visible
 
     // ids -> histogram + (bucket << 12 | index) entries; pass-1 ranks
     uint32_t e[ITEMS], rk[ITEMS];
@@ -247,7 +251,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
       uint32_t b = kSentinel;
       if (i < cnt) {
-        b = bufI[buf][i + shI];
+        b = pi.ok ? tI[i] : ids[begin + i];
         if (b >= nb) b = kSentinel;
         else atomicAdd(&hist[b], 1u);
       }
@@ -260,7 +264,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
     uint32_t hl = 0;
     for (uint32_t b = b0; b < b1; ++b) hl += hist[b];
-    uint32_t trun = radix_scan(dh, red, red64, hl);
+    uint32_t trun = radix_scan(dh, red64, hl);
     for (uint32_t b = b0; b < b1; ++b) {   // thread-owned buckets: no races
       const uint32_t h = hist[b];
       wbase[b] = cursor[b] - trun;
@@ -275,7 +279,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
     radix_rank<ITEMS>(e, kIdxBits + kRadixBits, dh, pm, rk);
     __syncthreads();
-    radix_scan(dh, red, red64, 0);
+    radix_scan(dh, red64, 0);
     __syncthreads();
     radix_scatter<ITEMS>(e, rk, kIdxBits + kRadixBits, dh, srtB);
     __syncthreads();
@@ -290,8 +294,8 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       uint64_t d = wbase[b] + s;
       if (dbg) d = begin + s;
       if (dbg != 1) {
-        dk[d] = bufK[buf][i + shK];
-        if constexpr (kHasV) dv[d] = bufV[buf][i + shV];
+        dk[d] = pk.ok ? tK[i] : sk[begin + i];
+        if constexpr (kHasV) dv[d] = pv.ok ? tV[i] : sv[begin + i];
       }
     }
     // advance (registers only, unless a new work item starts)
@@ -303,7 +307,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       cw = work[wi];
       tb = 0;
     }
-    __syncthreads();   // buffer `buf` may be refilled; wbase / srtB reusable
+    __syncthreads();   // stage `buf` may be refilled; wbase / srtB reusable
   }
 }
 

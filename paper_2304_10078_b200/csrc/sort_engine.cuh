@@ -31,24 +31,26 @@ inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
 }
 
 template <typename K, typename V, int TILE>
-inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
-                                uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
-                                uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st) {
+inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
+                                const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
+                                uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
+                                cudaStream_t st) {
   const size_t dsm = DistCfg<K, V, TILE>::smem_bytes(stride);
   auto kern = k_distribute<K, V, TILE>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
   const uint32_t grid = std::min<uint32_t>(nwork, 148 * kDistCtasPerSm);
-  kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
+  kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
                                         n_light, fixed_nb);
   check_launch();
 }
 
 // Stable scatter of every work item through its X row, by the u16 bucket
-// ids `ids` the count pass stored.
+// ids `ids` the count pass stored; n_src = element count of the sources.
 template <typename K, typename V>
 inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
                               uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
-                              uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st) {
+                              uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st,
+                              uint64_t n_src) {
   if (!nwork) return;
   static const int dbg = [] {
     const char* e = std::getenv("SS_DIST_DEBUG");
@@ -60,16 +62,16 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   if (stride >= kMaxDistBuckets) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
   switch (dist_tile_for<K, V>(stride)) {
     case 4096:
-      launch_distribute_t<K, V, 4096>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
-                                      fixed_nb, st);
+      launch_distribute_t<K, V, 4096>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
+                                      n_light, fixed_nb, st);
       break;
     case 2048:
-      launch_distribute_t<K, V, 2048>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
-                                      fixed_nb, st);
+      launch_distribute_t<K, V, 2048>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
+                                      n_light, fixed_nb, st);
       break;
     default:
-      launch_distribute_t<K, V, 1024>(sk, sv, ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
-                                      fixed_nb, st);
+      launch_distribute_t<K, V, 1024>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
+                                      n_light, fixed_nb, st);
   }
 }
 
@@ -314,7 +316,7 @@ struct SortEngine {
     // blocked distributing
     tr.begin(kPhDistribute);
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu,
-                            P.light_buckets, 0, st);
+                            P.light_buckets, 0, st, n);
     check_launch();
     tr.launched();
 

@@ -54,6 +54,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Bulk-copy plan for elements [begin, begin+cnt) of a T array of n_total
+// elements: one TMA copy of the 16-byte aligned superset of the range.
+// Element i of the range lands at index i + sh of the (16-byte aligned)
+// shared buffer.  When the superset would leave the array (misaligned array
+// start or end only), `ok` is false and consumers read global memory
+// directly for that tile -- the producer never does synchronous loads.
+template <typename T>
+struct Bulk16 {
+  const unsigned char* src;
+  uint32_t bytes, sh;
+  bool ok;
+  __device__ __forceinline__ Bulk16(const T* base, uint64_t n_total, uint64_t begin, uint32_t cnt) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(base), a1 = reinterpret_cast<uintptr_t>(base + n_total);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base + begin), e = reinterpret_cast<uintptr_t>(base + begin + cnt);
+    const uintptr_t lo = a & ~uintptr_t(15), hi = (e + 15) & ~uintptr_t(15);
+    ok = cnt > 0 && lo >= a0 && hi <= a1;
+    src = reinterpret_cast<const unsigned char*>(lo);
+    bytes = ok ? static_cast<uint32_t>(hi - lo) : 0u;
+    sh = static_cast<uint32_t>((a - lo) / sizeof(T));
+  }
+};
+
 // Split [begin, begin+cnt) of a T array into an unaligned head, a 16-byte
 // aligned bulk body and a tail.  `sh` is the element shift that makes the
 // body land 16-byte aligned in shared memory (element i of the range is

@@ -387,7 +387,7 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       auto kern = k_distribute<K, V, kTile>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
       kern<<<std::min<uint32_t>(nw, 148 * kDistCtasPerSm), kDistThreads, dsm, st>>>(
-          static_cast<const K*>(keys), static_cast<const V*>(values), pp.d_ids, static_cast<K*>(dst_keys),
+          static_cast<const K*>(keys), static_cast<const V*>(values), pp.d_ids, n, static_cast<K*>(dst_keys),
           static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, 0, parts);
     };
     auto withv = [&](auto kt) {
