@@ -238,116 +238,6 @@ struct WarpLeafSmem {
   __device__ __forceinline__ uint32_t* masks() { return reinterpret_cast<uint32_t*>(key_area); }
 };
 
-template <typename K, typename V>
-__global__ void __launch_bounds__(kLeafWarpWarps * 32)
-k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
-               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity) {
-  constexpr bool kHasV = ValTraits<V>::bytes > 0;
-  extern __shared__ __align__(16) unsigned char smem[];
-  WarpLeafSmem<K>& ws = reinterpret_cast<WarpLeafSmem<K>*>(smem)[warp_id()];
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
-  const uint32_t gw = blockIdx.x * kLeafWarpWarps + warp_id(), nw = gridDim.x * kLeafWarpWarps;
-  for (uint32_t l = gw; l < n_leaves; l += nw) {
-    const Leaf lf = leaves[l];
-    const uint32_t m = static_cast<uint32_t>(lf.size);
-    K key[kLeafWarpItems];
-    V val[kLeafWarpItems];
-#pragma unroll
-    for (int k = 0; k < kLeafWarpItems; ++k) {
-      const uint32_t i = lane + 32 * k;
-      if (i < m) {
-        key[k] = src_k[lf.lo + i];
-        if constexpr (kHasV) val[k] = src_v[lf.lo + i];
-        ws.keys()[i] = key[k];
-      }
-    }
-    const uint32_t cap = leaf_cap(m), mask = cap - 1;
-    for (uint32_t s = lane; s < cap; s += 32) {
-      ws.T[s] = kEmpty32;
-      ws.cell[s] = 0;
-      ws.gcnt[s] = 0;
-    }
-    __syncwarp();
-    uint32_t slot[kLeafWarpItems];
-#pragma unroll
-    for (int k = 0; k < kLeafWarpItems; ++k) {
-      const uint32_t i = lane + 32 * k;
-      slot[k] = 0;
-      if (i >= m) continue;
-      const uint32_t c = static_cast<uint32_t>(key_hash(key[k], identity != 0)) & mask;
-      atomicAdd(&ws.cell[c], 1u);
-      uint32_t s = c;
-      while (true) {
-        uint32_t t = ws.T[s];
-        if (t == kEmpty32) {
-          const uint32_t prev = atomicCAS(&ws.T[s], kEmpty32, i);
-          if (prev == kEmpty32) { ws.home[s] = static_cast<uint16_t>(c); break; }
-          t = prev;
-        }
-        if (ws.keys()[t] == key[k]) { atomicMin(&ws.T[s], i); break; }
-        s = (s + 1) & mask;
-      }
-      slot[k] = s;
-    }
-    __syncwarp();
-    // in-order ranks within groups (records i = lane + 32k, k ascending)
-    uint32_t* pmask = ws.masks();
-    for (uint32_t s = lane; s < cap; s += 32) pmask[s] = 0;
-    __syncwarp();
-    uint32_t rank[kLeafWarpItems];
-#pragma unroll
-    for (int k = 0; k < kLeafWarpItems; ++k) {
-      if (32 * k >= m) { rank[k] = 0; continue; }   // warp-uniform
-      const bool valid = lane + 32 * k < m;
-      if (valid) atomicOr(&pmask[slot[k]], 1u << lane);
-      __syncwarp();
-      const uint32_t peers = valid ? pmask[slot[k]] : 0u;
-      const uint32_t cnt = valid ? ws.gcnt[slot[k]] : 0u;
-      __syncwarp();
-      if (valid && lane == 31u - __clz(peers)) {
-        ws.gcnt[slot[k]] = static_cast<uint16_t>(cnt + __popc(peers));
-        pmask[slot[k]] = 0;
-      }
-      rank[k] = cnt + __popc(peers & lt);
-      __syncwarp();
-    }
-    // exclusive scan of records per cell (contiguous cells per lane)
-    {
-      const uint32_t per = cap / 32 > 0 ? cap / 32 : 1;
-      const uint32_t c0 = min(cap, lane * per), c1 = min(cap, c0 + per);
-      uint32_t local = 0;
-      for (uint32_t c = c0; c < c1; ++c) local += ws.cell[c];
-      uint32_t run = warp_incl_scan(local) - local;
-      for (uint32_t c = c0; c < c1; ++c) {
-        const uint32_t v = ws.cell[c];
-        ws.cell[c] = run;
-        run += v;
-      }
-    }
-    __syncwarp();
-    // group starts in (cell, first index) order
-    for (uint32_t s = lane; s < cap; s += 32) {
-      const uint32_t f = ws.T[s];
-      if (f == kEmpty32) continue;
-      const uint32_t c = ws.home[s];
-      uint32_t st = ws.cell[c];
-      for (uint32_t t = c; ws.T[t] != kEmpty32; t = (t + 1) & mask)
-        if (t != s && ws.home[t] == c && ws.T[t] < f) st += ws.gcnt[t];
-      ws.gstart[s] = static_cast<uint16_t>(st);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kLeafWarpItems; ++k) {
-      const uint32_t i = lane + 32 * k;
-      if (i >= m) continue;
-      const uint32_t pos = ws.gstart[slot[k]] + rank[k];
-      dst_k[lf.lo + pos] = key[k];
-      if constexpr (kHasV) dst_v[lf.lo + pos] = val[k];
-    }
-    __syncwarp();
-  }
-}
-
 __host__ inline size_t leaf_smem_bytes(int key_bytes, int val_bytes) {
   return static_cast<size_t>(kLeafSmemMax) * (key_bytes + val_bytes) +
          (5 * 2 * kLeafSmemMax + 2 * kLeafSmemMax) * 4 + 64;

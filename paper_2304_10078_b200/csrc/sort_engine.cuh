@@ -14,6 +14,7 @@
 
 #include "engine.cuh"
 #include "leaf.cuh"
+#include "leaf_warp.cuh"
 #include "multisplit.cuh"
 #include "sample.cuh"
 
