@@ -134,7 +134,7 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kLeafWarpWarps * 32)
+__global__ void __launch_bounds__(kLeafWarpWarps * 32, 3)
 k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
                V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
