@@ -134,7 +134,7 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kLeafWarpWarps * 32, 3)
+__global__ void __launch_bounds__(kLeafWarpWarps * 32)
 k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
                V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
@@ -152,10 +152,8 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       }
       continue;
     }
-    if (m <= 32) warp_leaf<K, V, 1>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws);
-    else if (m <= 64) warp_leaf<K, V, 2>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws);
-    else if (m <= 128) warp_leaf<K, V, 4>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws);
-    else warp_leaf<K, V, 8>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws);
+    // one instantiation: several inlined variants cost registers (occupancy)
+    warp_leaf<K, V, kLeafWarpItems>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws);
   }
 }
 
