@@ -107,7 +107,7 @@ def cpu_baseline(n_sample: int, repeats: int = 1):
 
     import oracle as O
     from oracle.datagen import gen_keys_values
-    ranks, _ = gen_keys_values("zipfian", ZIPF_S, n_sample, 64, seed=1)
+    ranks, _ = gen_keys_values("zipfian", ZIPF_S, n_sample, 64, seed=1, universe=UNIVERSE)
     keys = O.mix64_np(ranks - np.uint64(1))
     vals = np.arange(n_sample, dtype=np.uint64)
     P = O.OracleParams.derive(n_sample)
@@ -118,7 +118,7 @@ def cpu_baseline(n_sample: int, repeats: int = 1):
         times.append(time.perf_counter() - t0)
     t = min(times)
     return {"value": n_sample / t / 1e9, "unit": "Grecords/s", "cores": 1, "kind": "port",
-            "sample": f"semisort of {n_sample} records, Zipf s=1.2 ranks over [1, n_sample] hashed, "
+            "sample": f"semisort of {n_sample} records, Zipf s=1.2 ranks over [1, 1e9] hashed, "
                       f"value=index; reference algorithm restated in numpy (oracle/), single thread; "
                       f"best of {repeats}, {t:.2f} s"}
 
@@ -133,7 +133,7 @@ def reference_arm(args):
     import oracle as O
     from oracle.datagen import gen_keys_values
     n = args.ref_n
-    ranks, _ = gen_keys_values("zipfian", ZIPF_S, n, 64, seed=1)
+    ranks, _ = gen_keys_values("zipfian", ZIPF_S, n, 64, seed=1, universe=UNIVERSE)
     keys = O.mix64_np(ranks - np.uint64(1))
     vals = np.arange(n, dtype=np.uint64)
     P = O.OracleParams.derive(n)
@@ -149,7 +149,7 @@ def reference_arm(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"c2 semisort sample n={n} (bounded CPU sample of the 1e9 workload)",
-                       "key": "Zipf(1.2) rank over [1, n] -> mix64(rank-1)", "value": "index"},
+                       "key": "Zipf(1.2) rank over [1, 1e9] -> mix64(rank-1)", "value": "index"},
             "cpu_baseline": {"value": v, "unit": "Grecords/s", "cores": 1, "kind": "port",
                              "sample": f"{n} records per step, numpy restatement of the reference algorithm "
                                        "(oracle/), single thread (the reference's worker pool does not "
@@ -168,8 +168,8 @@ def main():
     ap.add_argument("--e2e-n", type=int, default=None, help="records for the e2e leg (default n)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-n", type=int, default=1 << 22)
-    ap.add_argument("--ref-n", type=int, default=1 << 22)
+    ap.add_argument("--cpu-n", type=int, default=1 << 25)
+    ap.add_argument("--ref-n", type=int, default=1 << 24)
     ap.add_argument("--validate", action="store_true", help="check the last output (O(n) device checks)")
     args = ap.parse_args()
 

@@ -43,8 +43,12 @@ def _zipf(rng, count, s, n):
     return out.astype(np.uint64)
 
 
-def gen_keys_values(family: str, param, n: int, key_width: int = 64, seed: int = 1):
-    """(keys, values) exactly as the reference ``generate`` for 32/64-bit keys."""
+def gen_keys_values(family: str, param, n: int, key_width: int = 64, seed: int = 1, universe=None):
+    """(keys, values) exactly as the reference ``generate`` for 32/64-bit keys.
+
+    ``universe`` overrides the Zipf rank range (the reference uses n,
+    datagen.py:118); bench.py uses it to draw a bounded sample of the
+    10^9-rank c2 workload."""
     kdt = np.uint32 if key_width == 32 else np.uint64
     keys = np.empty(n, dtype=kdt)
     vals = np.empty(n, dtype=kdt)
@@ -58,7 +62,7 @@ def gen_keys_values(family: str, param, n: int, key_width: int = 64, seed: int =
         elif family == "exponential":
             d = np.floor(rng.exponential(scale=1.0 / param, size=cnt)).astype(np.uint64)
         else:
-            d = _zipf(rng, cnt, float(param), n)
+            d = _zipf(rng, cnt, float(param), n if universe is None else int(universe))
         keys[lo:hi] = d.astype(kdt)
         top = 2**32 - 1 if key_width == 32 else 2**64 - 1
         vals[lo:hi] = rng.integers(0, top, size=cnt, dtype=kdt, endpoint=True)
