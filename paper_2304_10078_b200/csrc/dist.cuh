@@ -27,9 +27,6 @@
 
 namespace ss {
 
-constexpr int kDistThreads = 512;
-constexpr int kDistWarps = kDistThreads / 32;
-constexpr int kDistCtasPerSm = 1;
 constexpr int kRadixBits = 7;
 constexpr int kRadixBins = 1 << kRadixBits;
 constexpr uint32_t kIdxBits = 12;                              // tile index bits (tile <= 4096)
@@ -40,11 +37,15 @@ constexpr uint32_t kMaxDistBuckets = kSentinel;                // ids must stay 
 // stores, 2 store linearly (tile-contiguous).  Outputs are wrong unless 0.
 __device__ int g_dist_debug = 0;
 
-template <typename K, typename V, int TILE>
+// Launch shape: NT threads per CTA, STAGES input buffers, TILE records.
+template <typename K, typename V, int TILE, int NT = 512, int STAGES = 2>
 struct DistCfg {
   static constexpr int kValBytes = ValTraits<V>::bytes;
   static constexpr int kTile = TILE;
-  static constexpr int kItems = kTile / kDistThreads;
+  static constexpr int kThreads = NT;
+  static constexpr int kWarps = NT / 32;
+  static constexpr int kStages = STAGES;
+  static constexpr int kItems = kTile / kThreads;
   static constexpr size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   // +2 x (16 / element size) elements: the aligned superset of a tile
   static constexpr size_t kBufI = up16((static_cast<size_t>(kTile) + 16) * 2);
@@ -53,8 +54,8 @@ struct DistCfg {
       kValBytes ? up16((static_cast<size_t>(kTile) + 2 * (16 / kValBytes > 0 ? 16 / kValBytes : 1)) * kValBytes) : 0;
   static constexpr size_t kSet = kBufI + kBufK + kBufV;   // one pipeline stage
   static size_t smem_bytes(uint32_t stride) {
-    return 2 * kSet + 2 * static_cast<size_t>(kTile) * 4 + 2 * up16(static_cast<size_t>(stride) * 8) +
-           up16(static_cast<size_t>(stride) * 4) + 2 * kDistWarps * kRadixBins * 4 + 64;
+    return kStages * kSet + 2 * static_cast<size_t>(kTile) * 4 + 2 * up16(static_cast<size_t>(stride) * 8) +
+           up16(static_cast<size_t>(stride) * 4) + 2 * kWarps * kRadixBins * 4 + 64;
   }
 };
 
@@ -72,7 +73,7 @@ __host__ inline int dist_tile_for(uint32_t stride) {
 // w*(32*ITEMS) + k*32 + lane, digit = (e >> shift) & 127.  Leaves the warp's
 // digit counts in dh[w][*] and each item's rank among equal digits of its
 // warp (index order) in rk[k].
-template <int ITEMS>
+template <int ITEMS, int NW>
 __device__ __forceinline__ void radix_rank(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* pm,
                                            uint32_t (&rk)[ITEMS]) {
   const int w = warp_id(), lane = lane_id();
@@ -100,9 +101,11 @@ __device__ __forceinline__ void radix_rank(const uint32_t (&e)[ITEMS], int shift
 
 // (digit, warp)-major exclusive scan of dh in place: kPer entries per
 // thread.  `extra` (< 2^32 in total) is scanned alongside in the high half.
+template <int NW>
 __device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, unsigned long long* red64, uint32_t extra) {
-  constexpr int kEntries = kDistWarps * kRadixBins;
-  constexpr int kPer = kEntries / kDistThreads;
+  constexpr int kDistWarps = NW;
+  constexpr int kEntries = NW * kRadixBins;
+  constexpr int kPer = kEntries / (NW * 32);
   uint32_t v[kPer], s = 0;
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
@@ -138,26 +141,28 @@ __device__ __forceinline__ void radix_scatter(const uint32_t (&e)[ITEMS], const 
 // count pass.  Buckets kept: [0, nb) with nb = min(fixed_nb or
 // n_light + node.n_heavy, keep_below); others are dropped.  n_src: element
 // count of the source arrays (bounds of the aligned TMA supersets).
-template <typename K, typename V, int TILE>
-__global__ void __launch_bounds__(kDistThreads, kDistCtasPerSm)
+template <typename K, typename V, int TILE, int NT, int STAGES>
+__global__ void __launch_bounds__(NT, 512 / NT)
 k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
              K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
              const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
              uint32_t n_light, uint32_t fixed_nb) {
-  using Cfg = DistCfg<K, V, TILE>;
+  using Cfg = DistCfg<K, V, TILE, NT, STAGES>;
+  constexpr int kDistThreads = NT;
+  constexpr int kDistWarps = NT / 32;
   constexpr bool kHasV = Cfg::kValBytes > 0;
   constexpr int T = Cfg::kTile;
   constexpr int ITEMS = Cfg::kItems;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red64[33];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[STAGES];
 
   // stage b: [ids | keys | values] at smem + b * kSet (arithmetic keeps the
   // shared address space visible to the compiler: LDS, no local arrays)
   auto stI = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * Cfg::kSet); };
   auto stK = [&](int b) { return reinterpret_cast<K*>(smem + b * Cfg::kSet + Cfg::kBufI); };
   auto stV = [&](int b) { return reinterpret_cast<V*>(smem + b * Cfg::kSet + Cfg::kBufI + Cfg::kBufK); };
-  unsigned char* p = smem + 2 * Cfg::kSet;
+  unsigned char* p = smem + STAGES * Cfg::kSet;
   uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
   uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
   uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
@@ -191,8 +196,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   };
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
     fence_barrier_init();
   }
   // consumer state: current work item, cached in registers
@@ -212,17 +216,18 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     }
   };
   __syncthreads();
-  if (threadIdx.x == 0) {
-    issue(pw, ptb, 0);
-    padvance();
-  }
-  uint32_t nb = 0;
+  uint32_t nb = 0, issued = 0;
   bool fresh = true;
   for (uint32_t q = 0;; ++q) {
-    const int buf = q & 1;
-    if (threadIdx.x == 0 && pwi < n_work) {
-      issue(pw, ptb, buf ^ 1);
-      padvance();
+    const int buf = q % STAGES;
+    // keep STAGES tiles in flight (stage q % STAGES was released by the
+    // end-of-tile barrier of tile q - STAGES)
+    if (threadIdx.x == 0) {
+      while (issued < q + STAGES && pwi < n_work) {
+        issue(pw, ptb, issued % STAGES);
+        padvance();
+        ++issued;
+      }
     }
     if (fresh) {   // new subarray: its X row and bucket count
       nb = fixed_nb ? fixed_nb : n_light + nodes[cw.node].n_heavy;
@@ -241,7 +246,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     const uint16_t* tI = stI(buf) + pi.sh;
     const K* tK = stK(buf) + pk.sh;
     const V* tV = stV(buf) + pv.sh;
-    mbar_wait(&bars[buf], (q >> 1) & 1);
+    mbar_wait(&bars[buf], (q / STAGES) & 1);
     __syncthreads();   // cursors and zeroed histogram visible
 
     // ids -> histogram + (bucket << 12 | index) entries; pass-1 ranks
@@ -257,14 +262,14 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       }
       e[k] = (b << kIdxBits) | i;
     }
-    radix_rank<ITEMS>(e, kIdxBits, dh, pm, rk);
+    radix_rank<ITEMS, kDistWarps>(e, kIdxBits, dh, pm, rk);
     __syncthreads();
     // one fused scan: pass-1 digit bases and the histogram (bucket starts)
     const uint32_t per = (nb + kDistThreads - 1) / kDistThreads;
     const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
     uint32_t hl = 0;
     for (uint32_t b = b0; b < b1; ++b) hl += hist[b];
-    uint32_t trun = radix_scan(dh, red64, hl);
+    uint32_t trun = radix_scan<kDistWarps>(dh, red64, hl);
     for (uint32_t b = b0; b < b1; ++b) {   // thread-owned buckets: no races
       const uint32_t h = hist[b];
       wbase[b] = cursor[b] - trun;
@@ -277,9 +282,9 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
-    radix_rank<ITEMS>(e, kIdxBits + kRadixBits, dh, pm, rk);
+    radix_rank<ITEMS, kDistWarps>(e, kIdxBits + kRadixBits, dh, pm, rk);
     __syncthreads();
-    radix_scan(dh, red64, 0);
+    radix_scan<kDistWarps>(dh, red64, 0);
     __syncthreads();
     radix_scatter<ITEMS>(e, rk, kIdxBits + kRadixBits, dh, srtB);
     __syncthreads();

@@ -214,9 +214,9 @@ k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
 // warp-per-leaf base case (leaves up to kLeafWarpMax records)
 // ---------------------------------------------------------------------------
 //
-// Same chained-hash order as leaf_eq, with every step warp-synchronous:
-// records live in registers (up to 8 per lane, index lane + 32k), so
-// in-place leaves need no staging, and the in-order rank pass walks k.
+// Same chained-hash order as leaf_eq, computed as two stable counting
+// passes (leaf_warp.cuh).  Records live in registers (up to 8 per lane,
+// index lane + 32k), so in-place leaves need no staging.
 
 constexpr uint32_t kLeafWarpMax = 256;
 constexpr uint32_t kLeafWarpCap = 2 * kLeafWarpMax;
@@ -225,17 +225,12 @@ constexpr int kLeafWarpWarps = 8;
 
 template <typename K>
 struct WarpLeafSmem {
-  // key copies while inserting; afterwards the same words are the rank
-  // pass's 32-bit peer masks (cap <= kLeafWarpCap words)
-  alignas(8) unsigned char key_area[kLeafWarpCap * 4 > kLeafWarpMax * sizeof(K) ? kLeafWarpCap * 4
-                                                                                 : kLeafWarpMax * sizeof(K)];
-  uint32_t T[kLeafWarpCap];
-  uint32_t cell[kLeafWarpCap];
-  uint16_t home[kLeafWarpCap];
-  uint16_t gcnt[kLeafWarpCap];
-  uint16_t gstart[kLeafWarpCap];
-  __device__ __forceinline__ K* keys() { return reinterpret_cast<K*>(key_area); }
-  __device__ __forceinline__ uint32_t* masks() { return reinterpret_cast<uint32_t*>(key_area); }
+  alignas(16) uint32_t T[kLeafWarpCap];      // dedup table (first index); pass 2: per-cell cursors
+  alignas(16) uint32_t cnt[kLeafWarpMax];    // records per first index; pass 1: cursors
+  alignas(16) uint32_t mask[kLeafWarpCap];   // peer masks (zero between uses)
+  alignas(16) K keys[kLeafWarpMax];          // key copies for the dedup compares
+  uint16_t arr[kLeafWarpMax];                // pass 2: cell at each pass-1 position
+  uint16_t dest[kLeafWarpMax];               // pass 2: final position of each pass-1 position
 };
 
 __host__ inline size_t leaf_smem_bytes(int key_bytes, int val_bytes) {

@@ -12,6 +12,9 @@
 // back, leaves living in S are written to A by their base case.
 #pragma once
 
+#include <cstdio>
+#include <vector>
+
 #include "engine.cuh"
 #include "leaf.cuh"
 #include "leaf_warp.cuh"
@@ -26,23 +29,39 @@ constexpr uint32_t kSampleGridMax = 148;
 constexpr uint32_t kLeafSmemGrid = 148 * 3;
 constexpr uint32_t kLeafGlobalGridMax = 296;
 constexpr size_t kSampleSmem = kSampleSmemCap * 4;
+constexpr int kDistShapeDefault = 0;
 
 inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
   return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
 }
 
-template <typename K, typename V, int TILE>
+template <typename K, typename V, int TILE, int NT, int STAGES>
 inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
                                 const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
                                 uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
                                 cudaStream_t st) {
-  const size_t dsm = DistCfg<K, V, TILE>::smem_bytes(stride);
-  auto kern = k_distribute<K, V, TILE>;
+  const size_t dsm = DistCfg<K, V, TILE, NT, STAGES>::smem_bytes(stride);
+  auto kern = k_distribute<K, V, TILE, NT, STAGES>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-  const uint32_t grid = std::min<uint32_t>(nwork, 148 * kDistCtasPerSm);
-  kern<<<grid, kDistThreads, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
-                                        n_light, fixed_nb);
+  int per_sm = 0;
+  SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, dsm));
+  const uint32_t grid = std::min<uint32_t>(nwork, 148u * static_cast<uint32_t>(std::max(per_sm, 1)));
+  kern<<<grid, NT, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
+                              fixed_nb);
   check_launch();
+}
+
+// Distribute launch shapes (SS_DIST_SHAPE, measurement knob):
+//   0: 512 threads, 1 CTA/SM, double-buffered tiles of 4096 (or smaller)
+//   1: 256 threads, 2 CTAs/SM, single-buffered 2048-record tiles
+//   2: 256 threads, 2 CTAs/SM, double-buffered 1024-record tiles
+// Shapes 1/2 apply while two CTAs fit shared memory, else shape 0.
+inline int dist_shape() {
+  static const int v = [] {
+    const char* e = std::getenv("SS_DIST_SHAPE");
+    return e ? std::atoi(e) : kDistShapeDefault;
+  }();
+  return v;
 }
 
 // Stable scatter of every work item through its X row, by the u16 bucket
@@ -61,19 +80,43 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   }();
   (void)dbg;
   if (stride >= kMaxDistBuckets) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
-  switch (dist_tile_for<K, V>(stride)) {
-    case 4096:
-      launch_distribute_t<K, V, 4096>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
-                                      n_light, fixed_nb, st);
-      break;
-    case 2048:
-      launch_distribute_t<K, V, 2048>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
-                                      n_light, fixed_nb, st);
-      break;
-    default:
-      launch_distribute_t<K, V, 1024>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
-                                      n_light, fixed_nb, st);
+#define SS_DIST_ARGS sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light, fixed_nb, st
+  constexpr size_t kHalfSm = (228 * 1024) / 2 - 2048;   // two CTAs per SM
+  const int shape = dist_shape();
+  if (shape == 1 && DistCfg<K, V, 2048, 256, 1>::smem_bytes(stride) <= kHalfSm) {
+    launch_distribute_t<K, V, 2048, 256, 1>(SS_DIST_ARGS);
+    return;
   }
+  if (shape == 2 && DistCfg<K, V, 1024, 256, 2>::smem_bytes(stride) <= kHalfSm) {
+    launch_distribute_t<K, V, 1024, 256, 2>(SS_DIST_ARGS);
+    return;
+  }
+  switch (dist_tile_for<K, V>(stride)) {
+    case 4096: launch_distribute_t<K, V, 4096, 512, 2>(SS_DIST_ARGS); break;
+    case 2048: launch_distribute_t<K, V, 2048, 512, 2>(SS_DIST_ARGS); break;
+    default: launch_distribute_t<K, V, 1024, 512, 2>(SS_DIST_ARGS);
+  }
+#undef SS_DIST_ARGS
+}
+
+// Measurement knob (SS_LEAF_STATS=1): leaf size histogram per launch on stderr.
+inline void leaf_stats(const char* what, const Leaf* d_list, uint64_t count, cudaStream_t st) {
+  static const bool on = std::getenv("SS_LEAF_STATS") != nullptr;
+  if (!on || !count) return;
+  std::vector<Leaf> h(count);
+  SS_CUDA(cudaMemcpyAsync(h.data(), d_list, count * sizeof(Leaf), cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  uint64_t bins[12] = {}, recs = 0;
+  for (const Leaf& l : h) {
+    int b = 0;
+    while (b < 11 && (1ull << b) < l.size) ++b;
+    ++bins[b];
+    recs += l.size;
+  }
+  std::fprintf(stderr, "[leaf_stats] %s leaves=%llu records=%llu |", what, (unsigned long long)count,
+               (unsigned long long)recs);
+  for (int b = 0; b < 12; ++b) std::fprintf(stderr, " <=%llu:%llu", 1ull << b, (unsigned long long)bins[b]);
+  std::fprintf(stderr, "\n");
 }
 
 template <typename K, typename V>
@@ -158,6 +201,7 @@ struct SortEngine {
       run_leaves_global(tr, d_list, count, in_a, nullptr, 0);
       return;
     }
+    leaf_stats("warp", d_list, count, st);
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(cdiv(count, kLeafWarpWarps), 148 * 3));
     const size_t sm = sizeof(WarpLeafSmem<K>) * kLeafWarpWarps;
     SS_CUDA(cudaFuncSetAttribute(k_leaf_eq_warp<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
@@ -174,6 +218,7 @@ struct SortEngine {
       run_leaves_global(tr, d_list, count, in_a, nullptr, 0);
       return;
     }
+    leaf_stats("smem", d_list, count, st);
     const size_t smem = leaf_smem_bytes(sizeof(K), kHasV ? sizeof(V) : 0);
     auto kern = k_leaf_eq_smem<K, V>;
     SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -189,6 +234,7 @@ struct SortEngine {
   void run_leaves_global(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a, uint32_t* scr,
                          uint64_t words) {
     if (!count) return;
+    leaf_stats("global", d_list, count, st);
     uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, leafg_grid));
     if (!scr) { scr = d_leafscr; words = leafg_words; }
     else grid = 1;

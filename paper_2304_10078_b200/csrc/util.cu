@@ -383,10 +383,10 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       k_write_X<uint32_t, uint64_t><<<nd.n_grps, 256, 0, st>>>(pp.d_C, pp.d_node, pp.d_gn, nd.n_grps, pp.d_P, pp.d_X,
                                                                 pp.stride, 0, 0, parts, nullptr);
       constexpr int kTile = 2048;   // parts <= 4096 always fit this tile
-      const size_t dsm = DistCfg<K, V, kTile>::smem_bytes(pp.stride);
-      auto kern = k_distribute<K, V, kTile>;
+      const size_t dsm = DistCfg<K, V, kTile, 512, 2>::smem_bytes(pp.stride);
+      auto kern = k_distribute<K, V, kTile, 512, 2>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
-      kern<<<std::min<uint32_t>(nw, 148 * kDistCtasPerSm), kDistThreads, dsm, st>>>(
+      kern<<<std::min<uint32_t>(nw, 148), 512, dsm, st>>>(
           static_cast<const K*>(keys), static_cast<const V*>(values), pp.d_ids, n, static_cast<K*>(dst_keys),
           static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, 0, parts);
     };
