@@ -97,31 +97,44 @@ __global__ void k_heavy_fold(const Node* __restrict__ nodes, uint32_t n_nodes, c
   }
 }
 
-// Base fold of one leaf: groups in chained-hash order with count or sum.
+// Base fold of one leaf: groups in chained-hash order, (cell, first index)
+// (aggregate.py:239-264), with count or sum; leaf.cuh's dedup and passes.
 template <typename K, typename V, bool SUM>
 __device__ void leaf_fold(const K* rk, const V* rv, uint32_t m, bool identity, LeafArrays a, uint32_t* red,
                           K* out_k, uint64_t* out_a, uint32_t* g_out) {
   const uint32_t cap = leaf_cap(m);
-  leaf_group(rk, m, cap, identity, a);
-  if (SUM) {
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) a.gsum[s] = 0;
-    __syncthreads();
+  if (SUM)
+    for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) a.gsum[f] = 0;
+  const bool one_cell = leaf_dedup(rk, m, cap, identity, a);
+  if (SUM)
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
-      atomicAdd(&a.gsum[a.rslot[i]], static_cast<unsigned long long>(val_u64(rv[i])));
+      atomicAdd(&a.gsum[a.pos[i]], static_cast<unsigned long long>(val_u64(rv[i])));
+  // rank of each group (first index f) in (cell, f) order -> a.arr[f]
+  if (one_cell) {
+    for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) a.arr[f] = a.cnt[f] ? 1u : 0u;
+    __syncthreads();
+    leaf_scan(a.arr, m, red);
+  } else {
+    for (uint32_t c = threadIdx.x; c < cap; c += blockDim.x) a.T[c] = 0;
+    __syncthreads();
+    for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) {
+      if (!a.cnt[f]) continue;
+      const uint32_t c = static_cast<uint32_t>(key_hash(rk[f], identity)) & (cap - 1);
+      atomicAdd(&a.T[c], 1u);
+      a.arr[f] = c;
+    }
+    __syncthreads();
+    leaf_scan(a.T, cap, red);
+    if (warp_id() == 0) warp_walk(a.arr, a.cnt, m, a.mask, a.T, a.arr);
+    __syncthreads();
   }
-  for (uint32_t c = threadIdx.x; c < cap; c += blockDim.x) a.cell[c] = 0;
-  __syncthreads();
-  for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x)
-    if (a.T[s] != kEmpty32) atomicAdd(&a.cell[a.home[s]], 1u);
-  __syncthreads();
-  leaf_scan_cells(a.cell, cap, red);
-  leaf_group_starts(cap, a, true);
   uint32_t groups = 0;
-  for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-    if (a.T[s] == kEmpty32) continue;
-    const uint32_t g = a.gstart[s];
-    out_k[g] = rk[a.T[s]];
-    out_a[g] = SUM ? static_cast<uint64_t>(a.gsum[s]) : a.gcnt[s];
+  for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) {
+    const uint32_t c = a.cnt[f];
+    if (!c) continue;
+    const uint32_t g = a.arr[f];
+    out_k[g] = rk[f];
+    out_a[g] = SUM ? static_cast<uint64_t>(a.gsum[f]) : c;
     ++groups;
   }
   uint32_t tot;

@@ -1,18 +1,23 @@
 // Base cases (core.py:388-429; aggregate.py:239-264), one CTA per leaf.
 //
 // semisort= reproduces the reference's chained-hash order exactly: groups
-// (distinct keys) are emitted by (hash & (cap-1), first index), cap the
-// smallest power of two >= 2m, records of a group in input order
-// (core.py:388-422, pinned by test_core_ops.py:309-335).  We never sort:
-//   1. open-addressing table with home slot = the chained-hash cell; a
-//      group's entry holds its minimum record index (atomicMin);
-//   2. one warp walks the records in index order: match_any on the group
-//      slot gives each record its rank inside its group (stable);
-//   3. records per cell -> block scan -> cell starts;
-//   4. a group's start = its cell start + the sizes of the groups with the
-//      same home cell and a smaller first index (found in the probe run
-//      from the home cell, which linear probing keeps contiguous);
-//   5. record i goes to gstart[slot(i)] + rank(i).
+// (distinct keys) are emitted by (cell = hash & (cap-1), first index), cap
+// the smallest power of two >= 2m, records of a group in input order
+// (core.py:388-422, pinned by test_core_ops.py:309-335).  Computed as two
+// stable counting passes, O(m + cap), no comparison sort:
+//   1. dedup: lock-free linear probing from a multiplicative hash of the
+//      folded key hash; a group's slot keeps its minimum record index
+//      (atomicMin), which every record of the group then reads (fidx);
+//   2. pass 1: records per first index -> block scan -> one warp walks the
+//      records in index order, ranking peers of equal fidx (stable);
+//   3. pass 2 (skipped when all records share one cell -- the usual case
+//      below the root, where a leaf is one light bucket of every level above
+//      it and so shares the low b*depth hash bits): records per cell ->
+//      scan -> one warp walks the pass-1 sequence, ranking peers of equal
+//      cell (stable);
+//   4. record i goes to its final position.
+// The dedup probes do not start at the cell: with every record in one cell
+// that would be one cluster of all groups, quadratic in the group count.
 // Work arrays live in SMEM for leaves up to kLeafSmemMax records and in a
 // per-CTA global scratch (L2-resident) above that.
 #pragma once
@@ -27,14 +32,12 @@ constexpr uint32_t kLeafSmemMax = 1024;             // records per SMEM leaf
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 
 struct LeafArrays {
-  uint32_t* T;       // [cap] min record index of the slot's group
-  uint32_t* home;    // [cap] home cell of the slot's group
-  uint32_t* gcnt;    // [cap] group size (after the rank pass)
-  uint32_t* cell;    // [cap] records per cell -> cell start
-  uint32_t* gstart;  // [cap] group start
-  uint32_t* rslot;   // [m]
-  uint32_t* rank;    // [m]
-  unsigned long long* gsum;  // [cap] (aggregation only)
+  uint32_t* T;       // [cap] dedup table (min record index); pass 2: per-cell cursors
+  uint32_t* cnt;     // [m]   records per first index -> cursors
+  uint32_t* mask;    // [cap] peer masks (cap >= 2m)
+  uint32_t* pos;     // [m]   first index -> pass-1 position -> final position
+  uint32_t* arr;     // [m]   pass 2: cell at each pass-1 position -> final position
+  unsigned long long* gsum;  // [m] (aggregation only) sum per first index
 };
 
 __host__ __device__ inline uint32_t leaf_cap(uint64_t m) {
@@ -44,118 +47,134 @@ __host__ __device__ inline uint32_t leaf_cap(uint64_t m) {
 }
 
 __host__ __device__ inline uint64_t leaf_words(uint64_t m, bool agg) {
-  uint64_t cap = leaf_cap(m);
-  return 5 * cap + 2 * m + (agg ? 2 * cap : 0) + 8;
+  const uint64_t cap = leaf_cap(m);
+  return (2 * cap + 3 * m + (agg ? 2 * m + 2 : 0) + 16 + 3) & ~uint64_t(3);   // 16-byte multiple: per-CTA slices stay aligned
 }
 
 __device__ __forceinline__ LeafArrays leaf_arrays(uint32_t* base, uint32_t cap, uint32_t m, bool agg) {
   LeafArrays a;
   uint32_t* p = base;
-  if (agg) {
+  if (agg) {   // u64 first: keep it 8-byte aligned
     a.gsum = reinterpret_cast<unsigned long long*>(p);
-    p += 2 * cap;
+    p += 2 * m + 2;
   } else {
     a.gsum = nullptr;
   }
   a.T = p; p += cap;
-  a.home = p; p += cap;
-  a.gcnt = p; p += cap;
-  a.cell = p; p += cap;
-  a.gstart = p; p += cap;
-  a.rslot = p; p += m;
-  a.rank = p;
+  a.mask = p; p += cap;
+  a.cnt = p; p += m;
+  a.pos = p; p += m;
+  a.arr = p;
   return a;
 }
 
-// Steps 1-2: groups, per-record slot and in-group rank, group sizes.
-template <typename K>
-__device__ void leaf_group(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a) {
-  const uint32_t mask = cap - 1;
-  for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-    a.T[s] = kEmpty32;
-    a.gcnt[s] = 0;
-    a.cell[s] = 0;
-    a.gstart[s] = 0;   // peer-mask scratch of the rank pass
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const K k = rk[i];
-    const uint32_t c = static_cast<uint32_t>(key_hash(k, identity)) & mask;
-    atomicAdd(&a.cell[c], 1u);
-    uint32_t s = c;
-    while (true) {
-      uint32_t t = a.T[s];
-      if (t == kEmpty32) {
-        uint32_t prev = atomicCAS(&a.T[s], kEmpty32, i);
-        if (prev == kEmpty32) { a.home[s] = c; break; }
-        t = prev;
-      }
-      if (rk[t] == k) { atomicMin(&a.T[s], i); break; }
-      s = (s + 1) & mask;
-    }
-    a.rslot[i] = s;
-  }
-  __syncthreads();
-  if (warp_id() == 0) {
-    // in-order pass: peers of the same group among 32 consecutive records
-    // via atomicOr masks in a.gstart (not yet in use)
-    const uint32_t lt = lanemask_lt();
-    for (uint32_t base = 0; base < m; base += 32) {
-      const uint32_t i = base + lane_id();
-      const bool valid = i < m;
-      const uint32_t s = valid ? a.rslot[i] : 0;
-      if (valid) atomicOr(&a.gstart[s], 1u << lane_id());
-      __syncwarp();
-      uint32_t peers = 0, cnt = 0;
-      if (valid) {
-        peers = a.gstart[s];
-        cnt = a.gcnt[s];
-      }
-      __syncwarp();
-      if (valid) {
-        if (lane_id() == 31 - __clz(peers)) {
-          a.gcnt[s] = cnt + __popc(peers);
-          a.gstart[s] = 0;
-        }
-        a.rank[i] = cnt + __popc(peers & lt);
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
+// Probe start of the dedup table: top log2(cap) bits of a multiplicative
+// hash of the folded key hash (independent of the cell bits).
+__device__ __forceinline__ uint32_t leaf_probe(uint64_t h, uint32_t cap) {
+  return (static_cast<uint32_t>(h ^ (h >> 32)) * 0x9E3779B1u) >> (32 - (31 - __clz(cap)));
 }
 
-// Step 3: exclusive scan of cell[0..cap) in place (contiguous per thread).
-__device__ inline void leaf_scan_cells(uint32_t* cell, uint32_t cap, uint32_t* red) {
-  const uint32_t per = (cap + blockDim.x - 1) / blockDim.x;
-  const uint32_t c0 = min(cap, threadIdx.x * per), c1 = min(cap, c0 + per);
+// Stable in-order ranks of one 32-wide item: `key` < mask capacity; `cur`
+// holds each key's cursor and advances by the item's count.
+__device__ __forceinline__ uint32_t warp_rank_item(bool valid, uint32_t key, uint32_t* mask, uint32_t* cur,
+                                                   uint32_t lane, uint32_t lt) {
+  if (valid) atomicOr(&mask[key], 1u << lane);
+  __syncwarp();
+  const uint32_t peers = valid ? mask[key] : 0u;
+  const uint32_t base = valid ? cur[key] : 0u;
+  __syncwarp();
+  if (valid && lane == 31u - __clz(peers)) {
+    cur[key] = base + __popc(peers);
+    mask[key] = 0;
+  }
+  __syncwarp();
+  return base + __popc(peers & lt);
+}
+
+// One warp: out[p] = stable rank of key_of[p] (p in [0, L), in order) at the
+// cursors cur; invalid positions (valid_of[p] == 0 when given) are skipped.
+// out may alias key_of.
+__device__ __forceinline__ void warp_walk(const uint32_t* key_of, const uint32_t* valid_of, uint32_t L,
+                                          uint32_t* mask, uint32_t* cur, uint32_t* out) {
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t p = base + lane;
+    const bool valid = p < L && (valid_of == nullptr || valid_of[p] != 0);
+    const uint32_t k = valid ? key_of[p] : 0u;
+    const uint32_t r = warp_rank_item(valid, k, mask, cur, lane, lt);
+    if (valid) out[p] = r;
+  }
+}
+
+// Exclusive scan of a[0, L) in place (contiguous chunk per thread).
+__device__ inline void leaf_scan(uint32_t* a, uint32_t L, uint32_t* red) {
+  const uint32_t per = (L + blockDim.x - 1) / blockDim.x;
+  const uint32_t c0 = min(L, threadIdx.x * per), c1 = min(L, c0 + per);
   uint32_t local = 0;
-  for (uint32_t c = c0; c < c1; ++c) local += cell[c];
+  for (uint32_t c = c0; c < c1; ++c) local += a[c];
   uint32_t tot;
   uint32_t run = block_excl_scan<uint32_t>(local, red, tot);
   for (uint32_t c = c0; c < c1; ++c) {
-    uint32_t v = cell[c];
-    cell[c] = run;
+    const uint32_t v = a[c];
+    a[c] = run;
     run += v;
   }
   __syncthreads();
 }
 
-// Step 4: group starts in chained-hash order.  With count_groups, positions
-// are in units of groups (the aggregation output order) instead of records.
-__device__ inline void leaf_group_starts(uint32_t cap, LeafArrays a, bool count_groups) {
-  const uint32_t mask = cap - 1;
+// Step 1 + record counts per first index: a.pos[i] = first index of record
+// i's group, a.cnt[f] = size of the group whose first index is f (0 when f
+// is not a first index).  Returns whether every record shares one cell.
+template <typename K>
+__device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a) {
+  __shared__ uint32_t s_cmin, s_cmax;
+  const uint32_t cmask = cap - 1;
   for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-    const uint32_t f = a.T[s];
-    if (f == kEmpty32) continue;
-    const uint32_t c = a.home[s];
-    uint32_t st = a.cell[c];
-    for (uint32_t t = c; a.T[t] != kEmpty32; t = (t + 1) & mask) {
-      if (t != s && a.home[t] == c && a.T[t] < f) st += count_groups ? 1u : a.gcnt[t];
-    }
-    a.gstart[s] = st;
+    a.T[s] = kEmpty32;
+    a.mask[s] = 0;
+  }
+  for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) a.cnt[f] = 0;
+  if (threadIdx.x == 0) {
+    s_cmin = 0xFFFFFFFFu;
+    s_cmax = 0;
   }
   __syncthreads();
+  uint32_t cmin = 0xFFFFFFFFu, cmax = 0;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const K k = rk[i];
+    const uint64_t h = key_hash(k, identity);
+    const uint32_t c = static_cast<uint32_t>(h) & cmask;
+    cmin = min(cmin, c);
+    cmax = max(cmax, c);
+    uint32_t s = leaf_probe(h, cap);
+    while (true) {
+      uint32_t t = a.T[s];
+      if (t == kEmpty32) {
+        t = atomicCAS(&a.T[s], kEmpty32, i);
+        if (t == kEmpty32) break;
+      }
+      if (rk[t] == k) {
+        atomicMin(&a.T[s], i);
+        break;
+      }
+      s = (s + 1) & cmask;
+    }
+    a.pos[i] = s;
+  }
+  cmin = __reduce_min_sync(0xFFFFFFFFu, cmin);
+  cmax = __reduce_max_sync(0xFFFFFFFFu, cmax);
+  if (lane_id() == 0) {
+    atomicMin(&s_cmin, cmin);
+    atomicMax(&s_cmax, cmax);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint32_t f = a.T[a.pos[i]];
+    a.pos[i] = f;
+    atomicAdd(&a.cnt[f], 1u);
+  }
+  __syncthreads();
+  return s_cmin == s_cmax;
 }
 
 // Full semisort= leaf: records rk/rv (leaf-relative) -> ok/ov.
@@ -164,14 +183,33 @@ __device__ void leaf_eq(const K* rk, const V* rv, K* ok, V* ov, uint32_t m, bool
                         LeafArrays a, uint32_t* red) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   const uint32_t cap = leaf_cap(m);
-  leaf_group(rk, m, cap, identity, a);
-  leaf_scan_cells(a.cell, cap, red);
-  leaf_group_starts(cap, a, false);
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const uint32_t pos = a.gstart[a.rslot[i]] + a.rank[i];
-    ok[pos] = rk[i];
-    if constexpr (kHasV) ov[pos] = rv[i];
+  const bool one_cell = leaf_dedup(rk, m, cap, identity, a);
+  leaf_scan(a.cnt, m, red);
+  if (warp_id() == 0) warp_walk(a.pos, nullptr, m, a.mask, a.cnt, a.pos);   // pass 1
+  __syncthreads();
+  if (!one_cell) {   // pass 2
+    for (uint32_t c = threadIdx.x; c < cap; c += blockDim.x) a.T[c] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint32_t c = static_cast<uint32_t>(key_hash(rk[i], identity)) & (cap - 1);
+      atomicAdd(&a.T[c], 1u);
+      a.arr[a.pos[i]] = c;
+    }
+    __syncthreads();
+    leaf_scan(a.T, cap, red);
+    if (warp_id() == 0) warp_walk(a.arr, nullptr, m, a.mask, a.T, a.arr);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) a.pos[i] = a.arr[a.pos[i]];
   }
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint32_t p = a.pos[i];
+    ok[p] = rk[i];
+    if constexpr (kHasV) ov[p] = rv[i];
+  }
+}
+
+__host__ inline size_t leaf_smem_bytes(int key_bytes, int val_bytes) {
+  return static_cast<size_t>(kLeafSmemMax) * (key_bytes + val_bytes) + leaf_words(kLeafSmemMax, false) * 4 + 64;
 }
 
 // Leaves up to kLeafSmemMax records, fully in SMEM.  src_* is the side the
@@ -183,7 +221,6 @@ k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t red[33];
-  constexpr uint32_t kCap = 2 * kLeafSmemMax;
   K* rk = reinterpret_cast<K*>(smem);
   V* rv = reinterpret_cast<V*>(rk + kLeafSmemMax);
   uint32_t* work = reinterpret_cast<uint32_t*>(kHasV ? reinterpret_cast<unsigned char*>(rv + kLeafSmemMax)
@@ -203,8 +240,7 @@ k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       if constexpr (kHasV) rv[i] = src_v[lf.lo + i];
     }
     __syncthreads();
-    const uint32_t cap = leaf_cap(m);
-    LeafArrays a = leaf_arrays(work, cap <= kCap ? cap : kCap, m, false);
+    LeafArrays a = leaf_arrays(work, leaf_cap(m), m, false);
     leaf_eq(rk, rv, dst_k + lf.lo, dst_v + lf.lo, m, identity != 0, a, red);
     __syncthreads();
   }
@@ -232,11 +268,6 @@ struct WarpLeafSmem {
   uint16_t arr[kLeafWarpMax];                // pass 2: cell at each pass-1 position
   uint16_t dest[kLeafWarpMax];               // pass 2: final position of each pass-1 position
 };
-
-__host__ inline size_t leaf_smem_bytes(int key_bytes, int val_bytes) {
-  return static_cast<size_t>(kLeafSmemMax) * (key_bytes + val_bytes) +
-         (5 * 2 * kLeafSmemMax + 2 * kLeafSmemMax) * 4 + 64;
-}
 
 // Leaves with work arrays in global scratch (any size).  If the leaf lives
 // in A (in_a), it is first copied to the free S range, then S -> A.

@@ -46,23 +46,6 @@ __device__ __forceinline__ void warp_excl_scan_vec(uint32_t* a, uint32_t L) {
   }
 }
 
-// Stable in-order ranks of one 32-wide item: `key` < mask capacity; `cur`
-// holds each key's cursor and advances by the item's count.
-__device__ __forceinline__ uint32_t warp_rank_item(bool valid, uint32_t key, uint32_t* mask, uint32_t* cur,
-                                                   uint32_t lane, uint32_t lt) {
-  if (valid) atomicOr(&mask[key], 1u << lane);
-  __syncwarp();
-  const uint32_t peers = valid ? mask[key] : 0u;
-  const uint32_t base = valid ? cur[key] : 0u;
-  __syncwarp();
-  if (valid && lane == 31u - __clz(peers)) {
-    cur[key] = base + __popc(peers);
-    mask[key] = 0;
-  }
-  __syncwarp();
-  return base + __popc(peers & lt);
-}
-
 template <typename K, typename V, int ITEMS>
 __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                           K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t lo, uint32_t m,

@@ -26,7 +26,6 @@ namespace ss {
 constexpr uint64_t kTargetRows = 148 * 8;    // subarrays per level (~8 per SM)
 constexpr uint64_t kMinChunk = 4096;
 constexpr uint32_t kSampleGridMax = 148;
-constexpr uint32_t kLeafSmemGrid = 148 * 3;
 constexpr uint32_t kLeafGlobalGridMax = 296;
 constexpr size_t kSampleSmem = kSampleSmemCap * 4;
 constexpr int kDistShapeDefault = 0;
@@ -222,7 +221,9 @@ struct SortEngine {
     const size_t smem = leaf_smem_bytes(sizeof(K), kHasV ? sizeof(V) : 0);
     auto kern = k_leaf_eq_smem<K, V>;
     SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, kLeafSmemGrid));
+    int per_sm = 0;
+    SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, smem));
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
     kern<<<grid, kLeafThreads, smem, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v, d_list,
                                            static_cast<uint32_t>(count), identity);
     check_launch();
