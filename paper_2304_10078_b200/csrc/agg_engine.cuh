@@ -280,7 +280,7 @@ struct AggEngine {
     mh = std::max<uint32_t>(P.max_heavy, 1);
     const uint64_t alpha = P.base_case_cutoff;
     max_nodes = std::max<uint64_t>(1, n / alpha);
-    max_rows = kTargetRows + max_nodes;
+    max_rows = std::min<uint64_t>(kTargetRows, cdiv(n, kMinChunk)) + max_nodes;   // rows <= R / chunk + nodes
     max_grps = max_rows / kRowGroup + max_nodes + 1;
     max_leaves = std::max<uint64_t>(1, std::min<uint64_t>(n, max_nodes * P.light_buckets));
     s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
@@ -454,7 +454,7 @@ struct AggEngine {
 
     tr.begin(kPhDistribute);
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets,
-                            P.light_buckets, 0, st, n);
+                            P.light_buckets, 0, st, n, reinterpret_cast<uint32_t*>(d_misc + 7));
     tr.launched();
 
     tr.begin(kPhCopy);

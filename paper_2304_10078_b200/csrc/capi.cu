@@ -82,6 +82,7 @@ struct PhasePlan {
   uint64_t* d_P;
   uint64_t* d_off;
   uint64_t* d_heavy;
+  uint32_t* d_ctr;
   uint32_t* d_leafscr;
   uint64_t* d_samp;
   uint64_t leaf_words_n;
@@ -101,6 +102,7 @@ struct PhasePlan {
     d_P = a.take<uint64_t>(grps * stride);
     d_off = a.take<uint64_t>(stride + 1);
     d_heavy = a.take<uint64_t>(kMaxHeavyDevice);
+    d_ctr = a.take<uint32_t>(4);
     leaf_words_n = std::max(leaf_words(std::max<uint64_t>(n, 1), false), lt_leaf_words(n, key_bytes));
     d_leafscr = a.take<uint32_t>(leaf_words_n);
     s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
@@ -579,7 +581,7 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
       check_launch();
       launch_distribute<K, V>(sk, static_cast<const V*>(src_values), pp.d_ids, static_cast<K*>(dst_keys),
                               static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu,
-                              P.light_buckets, n_buckets, st, n);
+                              P.light_buckets, n_buckets, st, n, pp.d_ctr);
     });
     SS_CUDA(cudaStreamSynchronize(st));
   });

@@ -32,10 +32,15 @@ constexpr int kRadixBins = 1 << kRadixBits;
 constexpr uint32_t kIdxBits = 12;                              // tile index bits (tile <= 4096)
 constexpr uint32_t kSentinel = (1u << (2 * kRadixBits)) - 1;   // bucket sorting last
 constexpr uint32_t kMaxDistBuckets = kSentinel;                // ids must stay below
+// Row stride of the per-warp digit counters: 130 = 2 (mod 32) makes the
+// (digit, warp)-major scan reads conflict-free.
+constexpr int kDhStride = kRadixBins + 2;
 
 // Debug / measurement knob (SS_DIST_DEBUG): 0 normal, 1 skip the scattered
 // stores, 2 store linearly (tile-contiguous).  Outputs are wrong unless 0.
 __device__ int g_dist_debug = 0;
+// Phase profile (SS_DIST_DEBUG bit 4): cycles per phase summed over CTAs.
+__device__ unsigned long long g_dist_prof[12];   // [10] CTAs, [11] max cycles of one CTA
 
 // Launch shape: NT threads per CTA, STAGES input buffers, TILE records.
 template <typename K, typename V, int TILE, int NT = 512, int STAGES = 2>
@@ -55,7 +60,7 @@ struct DistCfg {
   static constexpr size_t kSet = kBufI + kBufK + kBufV;   // one pipeline stage
   static size_t smem_bytes(uint32_t stride) {
     return kStages * kSet + 2 * static_cast<size_t>(kTile) * 4 + 2 * up16(static_cast<size_t>(stride) * 8) +
-           up16(static_cast<size_t>(stride) * 4) + 2 * kWarps * kRadixBins * 4 + 64;
+           up16(static_cast<size_t>(stride) * 4) + 2 * kWarps * kDhStride * 4 + 64;
   }
 };
 
@@ -73,15 +78,28 @@ __host__ inline int dist_tile_for(uint32_t stride) {
 // w*(32*ITEMS) + k*32 + lane, digit = (e >> shift) & 127.  Leaves the warp's
 // digit counts in dh[w][*] and each item's rank among equal digits of its
 // warp (index order) in rk[k].
-template <int ITEMS, int NW>
+//
+// HW: a shared atomicAdd of 1 returns each lane its rank among the lanes
+// of the warp instruction that hit the same counter, in lane order, on
+// sm_100 (probed at load time by ss::hw_rank_ok(); HW is false if the probe
+// fails).  Otherwise peers come from shared atomicOr masks.
+template <int ITEMS, int NW, bool HW>
 __device__ __forceinline__ void radix_rank(const uint32_t (&e)[ITEMS], int shift, uint32_t* dh, uint32_t* pm,
                                            uint32_t (&rk)[ITEMS]) {
   const int w = warp_id(), lane = lane_id();
   const uint32_t lt = lanemask_lt();
-  uint32_t* mine = dh + w * kRadixBins;
-  uint32_t* mask = pm + w * kRadixBins;
+  uint32_t* mine = dh + w * kDhStride;
+  uint32_t* mask = pm + w * kDhStride;
   for (int i = lane; i < kRadixBins; i += 32) mine[i] = 0;
   __syncwarp();
+  if constexpr (HW) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      rk[k] = atomicAdd(&mine[(e[k] >> shift) & (kRadixBins - 1)], 1u);
+      __syncwarp();   // item k's increments precede item k+1's
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
@@ -110,7 +128,7 @@ __device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, unsigned long long*
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x * kPer + q;          // j = d * kDistWarps + w
-    v[q] = dh[(j % kDistWarps) * kRadixBins + j / kDistWarps];
+    v[q] = dh[(j % kDistWarps) * kDhStride + j / kDistWarps];
     s += v[q];
   }
   unsigned long long tot;
@@ -120,7 +138,7 @@ __device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, unsigned long long*
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x * kPer + q;
-    dh[(j % kDistWarps) * kRadixBins + j / kDistWarps] = run;
+    dh[(j % kDistWarps) * kDhStride + j / kDistWarps] = run;
     run += v[q];
   }
   return static_cast<uint32_t>(ex >> 32);
@@ -129,7 +147,7 @@ __device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, unsigned long long*
 template <int ITEMS>
 __device__ __forceinline__ void radix_scatter(const uint32_t (&e)[ITEMS], const uint32_t (&rk)[ITEMS], int shift,
                                               const uint32_t* dh, uint32_t* out) {
-  const uint32_t* mine = dh + warp_id() * kRadixBins;
+  const uint32_t* mine = dh + warp_id() * kDhStride;
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t d = (e[k] >> shift) & (kRadixBins - 1);
@@ -137,16 +155,34 @@ __device__ __forceinline__ void radix_scatter(const uint32_t (&e)[ITEMS], const 
   }
 }
 
+// Tile descriptor the producer publishes with each staged tile.
+struct TileDesc {
+  uint64_t begin;     // first record (absolute)
+  uint32_t cnt;       // records in the tile (0: no more work, exit)
+  uint32_t node;
+  uint64_t row;       // X row of the work item
+  uint32_t fresh;     // first tile of its work item
+  uint32_t pad;
+};
+
 // ids: u16 bucket id per source record (absolute index), written by the
 // count pass.  Buckets kept: [0, nb) with nb = min(fixed_nb or
 // n_light + node.n_heavy, keep_below); others are dropped.  n_src: element
 // count of the source arrays (bounds of the aligned TMA supersets).
-template <typename K, typename V, int TILE, int NT, int STAGES>
+//
+// Scheduling: thread 0 is the TMA producer.  It claims work items from the
+// global counter *ctr (zeroed by the launcher; work items are listed
+// longest first), keeps STAGES tiles in flight, and publishes each tile's
+// descriptor next to its data; the mbarrier phase that delivers the bytes
+// also orders the descriptor (arrive = release, try_wait = acquire).  A
+// work item's tiles stay on one CTA, in order: its X-row cursors advance
+// tile by tile, which keeps the scatter stable.
+template <typename K, typename V, int TILE, int NT, int STAGES, bool HW>
 __global__ void __launch_bounds__(NT, 512 / NT)
 k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
              K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
              const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
-             uint32_t n_light, uint32_t fixed_nb) {
+             uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr) {
   using Cfg = DistCfg<K, V, TILE, NT, STAGES>;
   constexpr int kDistThreads = NT;
   constexpr int kDistWarps = NT / 32;
@@ -156,6 +192,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red64[33];
   __shared__ __align__(8) uint64_t bars[STAGES];
+  __shared__ TileDesc sdesc[STAGES];
 
   // stage b: [ids | keys | values] at smem + b * kSet (arithmetic keeps the
   // shared address space visible to the compiler: LDS, no local arrays)
@@ -169,18 +206,49 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   uint64_t* wbase = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
   uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
   uint32_t* dh = reinterpret_cast<uint32_t*>(p);
-  uint32_t* pm = dh + kDistWarps * kRadixBins;
-  for (int i = threadIdx.x; i < kDistWarps * kRadixBins; i += blockDim.x) pm[i] = 0;
+  uint32_t* pm = dh + kDistWarps * kDhStride;
+  for (int i = threadIdx.x; i < kDistWarps * kDhStride; i += blockDim.x) pm[i] = 0;
   const int dbg = g_dist_debug;
   const int w = warp_id(), lane = lane_id();
 
-  auto next_valid = [&](uint32_t i) {
-    while (i < n_work && work[i].len == 0) i += gridDim.x;
+  // ---- producer (thread 0) ----
+  auto claim = [&]() {   // next non-empty work item, or n_work
+    uint32_t i;
+    do {
+      i = atomicAdd(ctr, 1u);
+    } while (i < n_work && work[i].len == 0);
     return i;
   };
-  auto issue = [&](const Work& wk, uint32_t tb, int b) {   // one thread, never blocks
-    const uint64_t begin = wk.begin + tb;
-    const uint32_t cnt = min(static_cast<uint32_t>(T), wk.len - tb);
+  uint32_t pwi = 0, ptb = 0, pnext = 0, issued = 0;
+  Work pw, pwn;
+  pw.len = 0;
+  pwn.len = 0;
+  bool pdone = false;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
+    fence_barrier_init();
+    pwi = claim();
+    if (pwi < n_work) pw = work[pwi];
+    pnext = claim();   // one item ahead: its descriptor load overlaps tiles
+    if (pnext < n_work) pwn = work[pnext];
+  }
+  auto issue_one = [&](int b) {   // stage b <- next tile, or the exit marker
+    if (pwi >= n_work) {
+      sdesc[b].cnt = 0;
+      mbar_arrive(&bars[b]);
+      pdone = true;
+      return;
+    }
+    const uint64_t begin = pw.begin + ptb;
+    const uint32_t cnt = min(static_cast<uint32_t>(T), pw.len - ptb);
+    TileDesc d;
+    d.begin = begin;
+    d.cnt = cnt;
+    d.node = pw.node;
+    d.row = pw.row;
+    d.fresh = ptb == 0;
+    d.pad = 0;
+    sdesc[b] = d;
     const Bulk16<uint16_t> bi(ids, n_src, begin, cnt);
     const Bulk16<K> bk(sk, n_src, begin, cnt);
     uint32_t bytes = bi.bytes + bk.bytes;
@@ -193,61 +261,63 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     if constexpr (kHasV) {
       if (bv.ok) bulk_g2s(stV(b), bv.src, bv.bytes, &bars[b]);
     }
-  };
-
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
-    fence_barrier_init();
-  }
-  // consumer state: current work item, cached in registers
-  uint32_t wi = next_valid(blockIdx.x);
-  if (wi >= n_work) return;
-  Work cw = work[wi];
-  uint32_t tb = 0;
-  // producer state (thread 0 only): next tile to stage
-  uint32_t pwi = wi, ptb = 0;
-  Work pw = cw;
-  auto padvance = [&]() {
     ptb += T;
-    if (ptb >= pw.len) {
-      pwi = next_valid(pwi + gridDim.x);
+    if (ptb >= pw.len) {   // advance to the prefetched item, prefetch the next
+      pwi = pnext;
+      pw = pwn;
       ptb = 0;
-      if (pwi < n_work) pw = work[pwi];
+      if (pwi < n_work) {
+        pnext = claim();
+        if (pnext < n_work) pwn = work[pnext];
+      }
     }
   };
   __syncthreads();
-  uint32_t nb = 0, issued = 0;
-  bool fresh = true;
+
+  uint32_t nb = 0;
+  const bool prof = (dbg & 4) && threadIdx.x == 0;
+  unsigned long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tlast = prof ? clock64() : 0;
+  auto mark = [&](int ph) {
+    if (prof) {
+      const unsigned long long t = clock64();
+      pacc[ph] += t - tlast;
+      tlast = t;
+    }
+  };
   for (uint32_t q = 0;; ++q) {
     const int buf = q % STAGES;
     // keep STAGES tiles in flight (stage q % STAGES was released by the
     // end-of-tile barrier of tile q - STAGES)
     if (threadIdx.x == 0) {
-      while (issued < q + STAGES && pwi < n_work) {
-        issue(pw, ptb, issued % STAGES);
-        padvance();
+      while (issued < q + STAGES && !pdone) {
+        issue_one(issued % STAGES);
         ++issued;
       }
     }
-    if (fresh) {   // new subarray: its X row and bucket count
-      nb = fixed_nb ? fixed_nb : n_light + nodes[cw.node].n_heavy;
+    mark(9);
+    mbar_wait(&bars[buf], (q / STAGES) & 1);
+    const TileDesc td = sdesc[buf];
+    if (td.cnt == 0) break;   // uniform: every thread read the same marker
+    const uint64_t begin = td.begin;
+    const uint32_t cnt = td.cnt;
+    if (td.fresh) {   // new work item: its X row and bucket count
+      nb = fixed_nb ? fixed_nb : n_light + nodes[td.node].n_heavy;
       if (nb > keep_below) nb = keep_below;
-      const uint64_t* xrow = X + cw.row * stride;
+      const uint64_t* xrow = X + td.row * stride;
       for (uint32_t b = threadIdx.x; b < nb; b += kDistThreads) {
         cursor[b] = xrow[b];
         hist[b] = 0;
       }
     }
-    const uint64_t begin = cw.begin + tb;
-    const uint32_t cnt = min(static_cast<uint32_t>(T), cw.len - tb);
     const Bulk16<uint16_t> pi(ids, n_src, begin, cnt);
     const Bulk16<K> pk(sk, n_src, begin, cnt);
     const Bulk16<V> pv(sv, n_src, begin, cnt);
     const uint16_t* tI = stI(buf) + pi.sh;
     const K* tK = stK(buf) + pk.sh;
     const V* tV = stV(buf) + pv.sh;
-    mbar_wait(&bars[buf], (q / STAGES) & 1);
+    mark(0);
     __syncthreads();   // cursors and zeroed histogram visible
+    mark(1);
 
     // ids -> histogram + (bucket << 12 | index) entries; pass-1 ranks
     uint32_t e[ITEMS], rk[ITEMS];
@@ -262,8 +332,9 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       }
       e[k] = (b << kIdxBits) | i;
     }
-    radix_rank<ITEMS, kDistWarps>(e, kIdxBits, dh, pm, rk);
+    radix_rank<ITEMS, kDistWarps, HW>(e, kIdxBits, dh, pm, rk);
     __syncthreads();
+    mark(2);
     // one fused scan: pass-1 digit bases and the histogram (bucket starts)
     const uint32_t per = (nb + kDistThreads - 1) / kDistThreads;
     const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
@@ -278,41 +349,76 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       trun += h;
     }
     __syncthreads();
+    mark(3);
     radix_scatter<ITEMS>(e, rk, kIdxBits, dh, srtA);
     __syncthreads();
+    mark(4);
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
-    radix_rank<ITEMS, kDistWarps>(e, kIdxBits + kRadixBits, dh, pm, rk);
+    radix_rank<ITEMS, kDistWarps, HW>(e, kIdxBits + kRadixBits, dh, pm, rk);
     __syncthreads();
+    mark(5);
     radix_scan<kDistWarps>(dh, red64, 0);
     __syncthreads();
+    mark(6);
     radix_scatter<ITEMS>(e, rk, kIdxBits + kRadixBits, dh, srtB);
     __syncthreads();
+    mark(7);
     // contiguous per-bucket runs out of the staged tile
+    if (pk.ok && (!kHasV || pv.ok) && !dbg) {
+      // batches of loads first (no branches between them), then the stores
+      constexpr int kB = ITEMS >= 4 ? 4 : ITEMS;
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t s = threadIdx.x + k * kDistThreads;
-      const uint32_t ent = srtB[s];
-      const uint32_t b = ent >> kIdxBits;
-      if (b == kSentinel) continue;
-      const uint32_t i = ent & ((1u << kIdxBits) - 1);
-      uint64_t d = wbase[b] + s;
-      if (dbg) d = begin + s;
-      if (dbg != 1) {
-        dk[d] = pk.ok ? tK[i] : sk[begin + i];
-        if constexpr (kHasV) dv[d] = pv.ok ? tV[i] : sv[begin + i];
+      for (int k0 = 0; k0 < ITEMS; k0 += kB) {
+        uint64_t dd[kB];
+        K kk[kB];
+        V vv[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const uint32_t s = threadIdx.x + (k0 + k) * kDistThreads;
+          const uint32_t ent = srtB[s];
+          const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
+          ok[k] = b != kSentinel;
+          dd[k] = wbase[ok[k] ? b : 0u] + s;
+          kk[k] = tK[i];
+          if constexpr (kHasV) vv[k] = tV[i];
+        }
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          if (ok[k]) {
+            dk[dd[k]] = kk[k];
+            if constexpr (kHasV) dv[dd[k]] = vv[k];
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t s = threadIdx.x + k * kDistThreads;
+        const uint32_t ent = srtB[s];
+        const uint32_t b = ent >> kIdxBits;
+        if (b == kSentinel) continue;
+        const uint32_t i = ent & ((1u << kIdxBits) - 1);
+        uint64_t d = wbase[b] + s;
+        if (dbg & 2) d = begin + s;
+        if (!(dbg & 1)) {
+          dk[d] = pk.ok ? tK[i] : sk[begin + i];
+          if constexpr (kHasV) dv[d] = pv.ok ? tV[i] : sv[begin + i];
+        }
       }
     }
-    // advance (registers only, unless a new work item starts)
-    tb += T;
-    fresh = tb >= cw.len;
-    if (fresh) {
-      wi = next_valid(wi + gridDim.x);
-      if (wi >= n_work) break;
-      cw = work[wi];
-      tb = 0;
+    __syncthreads();   // stage `buf` may be refilled; wbase / srtB / sdesc reusable
+    mark(8);
+  }
+  if (prof) {
+    unsigned long long tot = 0;
+    for (int p = 0; p < 10; ++p) {
+      atomicAdd(&g_dist_prof[p], pacc[p]);
+      tot += pacc[p];
     }
-    __syncthreads();   // stage `buf` may be refilled; wbase / srtB reusable
+    atomicAdd(&g_dist_prof[10], 1ull);
+    atomicMax(&g_dist_prof[11], tot);
   }
 }
 

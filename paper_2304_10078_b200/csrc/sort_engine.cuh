@@ -19,11 +19,12 @@
 #include "leaf.cuh"
 #include "leaf_warp.cuh"
 #include "multisplit.cuh"
+#include "probe.cuh"
 #include "sample.cuh"
 
 namespace ss {
 
-constexpr uint64_t kTargetRows = 148 * 8;    // subarrays per level (~8 per SM)
+constexpr uint64_t kTargetRows = 148 * 32;   // subarrays per level (~32 per SM: dynamic scheduling granularity)
 constexpr uint64_t kMinChunk = 4096;
 constexpr uint32_t kSampleGridMax = 148;
 constexpr uint32_t kLeafGlobalGridMax = 296;
@@ -34,19 +35,20 @@ inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
   return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
 }
 
-template <typename K, typename V, int TILE, int NT, int STAGES>
+template <typename K, typename V, int TILE, int NT, int STAGES, bool HW>
 inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
                                 const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
                                 uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
-                                cudaStream_t st) {
+                                cudaStream_t st, uint32_t* ctr) {
   const size_t dsm = DistCfg<K, V, TILE, NT, STAGES>::smem_bytes(stride);
-  auto kern = k_distribute<K, V, TILE, NT, STAGES>;
+  auto kern = k_distribute<K, V, TILE, NT, STAGES, HW>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
   int per_sm = 0;
   SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, dsm));
   const uint32_t grid = std::min<uint32_t>(nwork, 148u * static_cast<uint32_t>(std::max(per_sm, 1)));
+  SS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
   kern<<<grid, NT, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
-                              fixed_nb);
+                              fixed_nb, ctr);
   check_launch();
 }
 
@@ -64,12 +66,13 @@ inline int dist_shape() {
 }
 
 // Stable scatter of every work item through its X row, by the u16 bucket
-// ids `ids` the count pass stored; n_src = element count of the sources.
+// ids `ids` the count pass stored; n_src = element count of the sources;
+// ctr = one workspace word (the dynamic work counter, zeroed here).
 template <typename K, typename V>
 inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
                               uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
                               uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st,
-                              uint64_t n_src) {
+                              uint64_t n_src, uint32_t* ctr) {
   if (!nwork) return;
   static const int dbg = [] {
     const char* e = std::getenv("SS_DIST_DEBUG");
@@ -79,23 +82,44 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   }();
   (void)dbg;
   if (stride >= kMaxDistBuckets) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
-#define SS_DIST_ARGS sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light, fixed_nb, st
+#define SS_DIST_ARGS \
+  sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light, fixed_nb, st, ctr
   constexpr size_t kHalfSm = (228 * 1024) / 2 - 2048;   // two CTAs per SM
   const int shape = dist_shape();
-  if (shape == 1 && DistCfg<K, V, 2048, 256, 1>::smem_bytes(stride) <= kHalfSm) {
-    launch_distribute_t<K, V, 2048, 256, 1>(SS_DIST_ARGS);
-    return;
-  }
-  if (shape == 2 && DistCfg<K, V, 1024, 256, 2>::smem_bytes(stride) <= kHalfSm) {
-    launch_distribute_t<K, V, 1024, 256, 2>(SS_DIST_ARGS);
-    return;
-  }
-  switch (dist_tile_for<K, V>(stride)) {
-    case 4096: launch_distribute_t<K, V, 4096, 512, 2>(SS_DIST_ARGS); break;
-    case 2048: launch_distribute_t<K, V, 2048, 512, 2>(SS_DIST_ARGS); break;
-    default: launch_distribute_t<K, V, 1024, 512, 2>(SS_DIST_ARGS);
+  if (hw_rank_ok()) {
+    if (shape == 1 && DistCfg<K, V, 2048, 256, 1>::smem_bytes(stride) <= kHalfSm) {
+      launch_distribute_t<K, V, 2048, 256, 1, true>(SS_DIST_ARGS);
+    } else {
+      switch (dist_tile_for<K, V>(stride)) {
+        case 4096: launch_distribute_t<K, V, 4096, 512, 2, true>(SS_DIST_ARGS); break;
+        case 2048: launch_distribute_t<K, V, 2048, 512, 2, true>(SS_DIST_ARGS); break;
+        default: launch_distribute_t<K, V, 1024, 512, 2, true>(SS_DIST_ARGS);
+      }
+    }
+  } else {
+    switch (dist_tile_for<K, V>(stride)) {
+      case 4096: launch_distribute_t<K, V, 4096, 512, 2, false>(SS_DIST_ARGS); break;
+      case 2048: launch_distribute_t<K, V, 2048, 512, 2, false>(SS_DIST_ARGS); break;
+      default: launch_distribute_t<K, V, 1024, 512, 2, false>(SS_DIST_ARGS);
+    }
   }
 #undef SS_DIST_ARGS
+  if (dbg & 4) {   // phase profile of this launch on stderr
+    unsigned long long pr[12];
+    SS_CUDA(cudaStreamSynchronize(st));
+    SS_CUDA(cudaMemcpyFromSymbol(pr, g_dist_prof, sizeof(pr)));
+    static const char* names[10] = {"top", "wait", "rank1", "scan1", "scat1", "rank2", "scan2", "scat2", "write",
+                                    "issue"};
+    unsigned long long tot = 0;
+    for (int p = 0; p < 10; ++p) tot += pr[p];
+    std::fprintf(stderr, "[dist_prof] nwork=%u ctas=%llu cyc/cta avg=%.0f max=%llu |", nwork, pr[10],
+                 double(tot) / double(pr[10] ? pr[10] : 1), pr[11]);
+    for (int p = 0; p < 10; ++p)
+      std::fprintf(stderr, " %s %.1f%%", names[p], 100.0 * double(pr[p]) / double(tot ? tot : 1));
+    std::fprintf(stderr, "\n");
+    const unsigned long long zero[12] = {};
+    SS_CUDA(cudaMemcpyToSymbol(g_dist_prof, zero, sizeof(zero)));
+  }
 }
 
 // Measurement knob (SS_LEAF_STATS=1): leaf size histogram per launch on stderr.
@@ -148,6 +172,7 @@ struct SortEngine {
   uint64_t* d_off = nullptr;
   uint32_t* d_ccnt = nullptr;
   uint64_t* d_misc = nullptr;
+  uint32_t* d_ctr = nullptr;   // distribute work counter
   Leaf* d_leaf_w = nullptr;   // warp leaves (<= kLeafWarpMax)
   Leaf* d_leaf_s = nullptr;   // SMEM CTA leaves (<= kLeafSmemMax)
   Leaf* d_leaf_g = nullptr;   // global-scratch CTA leaves
@@ -160,7 +185,7 @@ struct SortEngine {
     stride = even_stride(P);
     const uint64_t alpha = P.base_case_cutoff;
     max_nodes = std::max<uint64_t>(1, n / alpha);
-    max_rows = kTargetRows + max_nodes;
+    max_rows = std::min<uint64_t>(kTargetRows, cdiv(n, kMinChunk)) + max_nodes;   // rows <= R / chunk + nodes
     max_grps = max_rows / kRowGroup + max_nodes + 1;
     max_leaves = std::max<uint64_t>(1, std::min<uint64_t>(n, max_nodes * P.light_buckets));
     s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
@@ -183,6 +208,7 @@ struct SortEngine {
     d_off = a.take<uint64_t>(max_nodes * (stride + 1));
     d_ccnt = a.take<uint32_t>(max_nodes * 4);
     d_misc = a.take<uint64_t>(8);
+    d_ctr = a.take<uint32_t>(4);
     d_leaf_w = a.take<Leaf>(max_leaves);
     d_leaf_s = a.take<Leaf>(max_leaves);
     d_leaf_g = a.take<Leaf>(max_leaves);
@@ -321,6 +347,8 @@ struct SortEngine {
     }
     if (work.size() > max_rows || grp_node.size() > max_grps || nn > max_nodes)
       throw Fail(SS_ERR_RESOURCE, "level plan exceeds workspace bounds");
+    // longest first: the distribute kernel claims work items dynamically
+    std::stable_sort(work.begin(), work.end(), [](const Work& x, const Work& y) { return x.len > y.len; });
     const uint32_t nwork = static_cast<uint32_t>(work.size());
     const uint32_t ngrp = static_cast<uint32_t>(grp_node.size());
     tr.begin(kPhOther);
@@ -364,7 +392,7 @@ struct SortEngine {
     // blocked distributing
     tr.begin(kPhDistribute);
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu,
-                            P.light_buckets, 0, st, n);
+                            P.light_buckets, 0, st, n, d_ctr);
     check_launch();
     tr.launched();
 

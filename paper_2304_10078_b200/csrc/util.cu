@@ -208,6 +208,7 @@ struct PartPlan {
   uint64_t* d_P;
   uint64_t* d_off;
   uint16_t* d_ids;
+  uint32_t* d_ctr;
   void carve(Arena& a, uint64_t n, uint32_t parts) {
     stride = (parts + 1) & ~1u;
     rows = std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(n, 4096)));
@@ -220,6 +221,7 @@ struct PartPlan {
     d_P = a.take<uint64_t>(grps * stride);
     d_off = a.take<uint64_t>(stride + 1);
     d_ids = a.take<uint16_t>(n);
+    d_ctr = a.take<uint32_t>(4);
   }
 };
 
@@ -384,11 +386,13 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
                                                                 pp.stride, 0, 0, parts, nullptr);
       constexpr int kTile = 2048;   // parts <= 4096 always fit this tile
       const size_t dsm = DistCfg<K, V, kTile, 512, 2>::smem_bytes(pp.stride);
-      auto kern = k_distribute<K, V, kTile, 512, 2>;
+      auto kern = k_distribute<K, V, kTile, 512, 2, false>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
+      SS_CUDA(cudaMemsetAsync(pp.d_ctr, 0, sizeof(uint32_t), st));
       kern<<<std::min<uint32_t>(nw, 148), 512, dsm, st>>>(
           static_cast<const K*>(keys), static_cast<const V*>(values), pp.d_ids, n, static_cast<K*>(dst_keys),
-          static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, 0, parts);
+          static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, 0, parts,
+          pp.d_ctr);
     };
     auto withv = [&](auto kt) {
       using K = decltype(kt);
