@@ -117,6 +117,31 @@ __device__ __forceinline__ void radix_rank(const uint32_t (&e)[ITEMS], int shift
   }
 }
 
+// Barrier of the NW consumer warps only (named barrier 1): the producer
+// warp never joins it.
+template <int NW>
+__device__ __forceinline__ void csync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+}
+
+// Exclusive scan over the NW consumer warps, one value per thread, with a
+// single barrier: every warp rescans the NW warp totals itself.  `red`
+// (NW entries) must not be rewritten before all warps have read it (the
+// callers separate two scans by at least one barrier).
+template <int NW>
+__device__ __forceinline__ unsigned long long cscan_u64(unsigned long long v, unsigned long long* red,
+                                                        unsigned long long& total) {
+  const int w = warp_id(), lane = lane_id();
+  const unsigned long long inc = warp_incl_scan(v);
+  if (lane == 31) red[w] = inc;
+  csync<NW>();
+  const unsigned long long x = lane < NW ? red[lane] : 0ull;
+  const unsigned long long xi = warp_incl_scan(x);
+  total = __shfl_sync(0xffffffffu, xi, NW - 1);
+  const unsigned long long before = __shfl_sync(0xffffffffu, xi - x, w);
+  return before + inc - v;
+}
+
 // (digit, warp)-major exclusive scan of dh in place: kPer entries per
 // thread.  `extra` (< 2^32 in total) is scanned alongside in the high half.
 template <int NW>
@@ -133,7 +158,7 @@ __device__ __forceinline__ uint32_t radix_scan(uint32_t* dh, unsigned long long*
   }
   unsigned long long tot;
   const unsigned long long packed = (static_cast<unsigned long long>(extra) << 32) | s;
-  const unsigned long long ex = block_excl_scan<unsigned long long>(packed, red64, tot);
+  const unsigned long long ex = cscan_u64<NW>(packed, red64, tot);
   uint32_t run = static_cast<uint32_t>(ex);
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
@@ -165,53 +190,23 @@ struct TileDesc {
   uint32_t pad;
 };
 
-// ids: u16 bucket id per source record (absolute index), written by the
-// count pass.  Buckets kept: [0, nb) with nb = min(fixed_nb or
-// n_light + node.n_heavy, keep_below); others are dropped.  n_src: element
-// count of the source arrays (bounds of the aligned TMA supersets).
-//
-// Scheduling: thread 0 is the TMA producer.  It claims work items from the
-// global counter *ctr (zeroed by the launcher; work items are listed
-// longest first), keeps STAGES tiles in flight, and publishes each tile's
-// descriptor next to its data; the mbarrier phase that delivers the bytes
-// also orders the descriptor (arrive = release, try_wait = acquire).  A
-// work item's tiles stay on one CTA, in order: its X-row cursors advance
-// tile by tile, which keeps the scatter stable.
-template <typename K, typename V, int TILE, int NT, int STAGES, bool HW>
-__global__ void __launch_bounds__(NT, 512 / NT)
-k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
-             K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
-             const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
-             uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr) {
-  using Cfg = DistCfg<K, V, TILE, NT, STAGES>;
-  constexpr int kDistThreads = NT;
-  constexpr int kDistWarps = NT / 32;
+// Producer (one thread of the producer warp): claims work items from the
+// global counter *ctr (zeroed by the launcher; items listed longest first),
+// keeps Cfg::kStages tiles in flight, publishes each tile's descriptor next
+// to its data (the mbarrier phase that delivers the bytes also orders the
+// descriptor: arrive = release, try_wait = acquire), and ends with an exit
+// marker (cnt = 0).  A work item's tiles stay on one CTA, in order.
+template <typename K, typename V, typename Cfg>
+__device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __restrict__ sk, const V* __restrict__ sv,
+                                              const uint16_t* __restrict__ ids, uint64_t n_src,
+                                              const Work* __restrict__ work, uint32_t n_work, uint32_t* ctr,
+                                              uint64_t* full, uint64_t* empty, TileDesc* sdesc, int dbg) {
   constexpr bool kHasV = Cfg::kValBytes > 0;
   constexpr int T = Cfg::kTile;
-  constexpr int ITEMS = Cfg::kItems;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long red64[33];
-  __shared__ __align__(8) uint64_t bars[STAGES];
-  __shared__ TileDesc sdesc[STAGES];
-
-  // stage b: [ids | keys | values] at smem + b * kSet (arithmetic keeps the
-  // shared address space visible to the compiler: LDS, no local arrays)
+  constexpr int STAGES = Cfg::kStages;
   auto stI = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * Cfg::kSet); };
   auto stK = [&](int b) { return reinterpret_cast<K*>(smem + b * Cfg::kSet + Cfg::kBufI); };
   auto stV = [&](int b) { return reinterpret_cast<V*>(smem + b * Cfg::kSet + Cfg::kBufI + Cfg::kBufK); };
-  unsigned char* p = smem + STAGES * Cfg::kSet;
-  uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
-  uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
-  uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
-  uint64_t* wbase = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
-  uint32_t* dh = reinterpret_cast<uint32_t*>(p);
-  uint32_t* pm = dh + kDistWarps * kDhStride;
-  for (int i = threadIdx.x; i < kDistWarps * kDhStride; i += blockDim.x) pm[i] = 0;
-  const int dbg = g_dist_debug;
-  const int w = warp_id(), lane = lane_id();
-
-  // ---- producer (thread 0) ----
   auto claim = [&]() {   // next non-empty work item, or n_work
     uint32_t i;
     do {
@@ -219,24 +214,21 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     } while (i < n_work && work[i].len == 0);
     return i;
   };
-  uint32_t pwi = 0, ptb = 0, pnext = 0, issued = 0;
+  const uint64_t pol = l2_evict_first_policy();
+  const bool l2_hint = !(dbg & 8);   // SS_DIST_DEBUG bit 8: plain loads (measurement)
+  uint32_t pwi = claim(), ptb = 0;
   Work pw, pwn;
   pw.len = 0;
   pwn.len = 0;
-  bool pdone = false;
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
-    fence_barrier_init();
-    pwi = claim();
-    if (pwi < n_work) pw = work[pwi];
-    pnext = claim();   // one item ahead: its descriptor load overlaps tiles
-    if (pnext < n_work) pwn = work[pnext];
-  }
-  auto issue_one = [&](int b) {   // stage b <- next tile, or the exit marker
-    if (pwi >= n_work) {
+  if (pwi < n_work) pw = work[pwi];
+  uint32_t pnext = pwi < n_work ? claim() : n_work;   // one item ahead
+  if (pnext < n_work) pwn = work[pnext];
+  for (uint32_t j = 0;; ++j) {
+    const int b = j % STAGES;
+    if (j >= STAGES) mbar_wait(&empty[b], ((j / STAGES) - 1) & 1);   // tile j - STAGES consumed
+    if (pwi >= n_work) {   // exit marker
       sdesc[b].cnt = 0;
-      mbar_arrive(&bars[b]);
-      pdone = true;
+      mbar_arrive(&full[b]);
       return;
     }
     const uint64_t begin = pw.begin + ptb;
@@ -255,11 +247,19 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     Bulk16<V> bv(sv, n_src, begin, cnt);
     if constexpr (kHasV) bytes += bv.bytes;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&bars[b], bytes);
-    if (bi.ok) bulk_g2s(stI(b), bi.src, bi.bytes, &bars[b]);
-    if (bk.ok) bulk_g2s(stK(b), bk.src, bk.bytes, &bars[b]);
-    if constexpr (kHasV) {
-      if (bv.ok) bulk_g2s(stV(b), bv.src, bv.bytes, &bars[b]);
+    mbar_arrive_expect_tx(&full[b], bytes);
+    if (l2_hint) {
+      if (bi.ok) bulk_g2s_hint(stI(b), bi.src, bi.bytes, &full[b], pol);
+      if (bk.ok) bulk_g2s_hint(stK(b), bk.src, bk.bytes, &full[b], pol);
+      if constexpr (kHasV) {
+        if (bv.ok) bulk_g2s_hint(stV(b), bv.src, bv.bytes, &full[b], pol);
+      }
+    } else {
+      if (bi.ok) bulk_g2s(stI(b), bi.src, bi.bytes, &full[b]);
+      if (bk.ok) bulk_g2s(stK(b), bk.src, bk.bytes, &full[b]);
+      if constexpr (kHasV) {
+        if (bv.ok) bulk_g2s(stV(b), bv.src, bv.bytes, &full[b]);
+      }
     }
     ptb += T;
     if (ptb >= pw.len) {   // advance to the prefetched item, prefetch the next
@@ -271,8 +271,67 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
         if (pnext < n_work) pwn = work[pnext];
       }
     }
-  };
+  }
+}
+
+// ids: u16 bucket id per source record (absolute index), written by the
+// count pass.  Buckets kept: [0, nb) with nb = min(fixed_nb or
+// n_light + node.n_heavy, keep_below); others are dropped.  n_src: element
+// count of the source arrays (bounds of the aligned TMA supersets).
+//
+// NT consumer threads + one producer warp (dist_producer).  A work item's
+// tiles stay on one CTA, in order: its X-row cursors advance tile by tile,
+// which keeps the scatter stable.  This two-pass LSD kernel is the general
+// path; dist1.cuh's single-pass kernel serves when its tables fit.
+template <typename K, typename V, int TILE, int NT, int STAGES, bool HW>
+__global__ void __launch_bounds__(NT + 32, 1)   // 17 warps: one sub-partition holds 5 -> <= 96 registers
+
+k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
+             K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
+             const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
+             uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr) {
+  using Cfg = DistCfg<K, V, TILE, NT, STAGES>;
+  constexpr int kDistThreads = NT;
+  constexpr int kDistWarps = NT / 32;
+  constexpr bool kHasV = Cfg::kValBytes > 0;
+  constexpr int T = Cfg::kTile;
+  constexpr int ITEMS = Cfg::kItems;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long red64[33];
+  __shared__ __align__(8) uint64_t full[STAGES];    // tile bytes landed (producer arrive + TMA tx)
+  __shared__ __align__(8) uint64_t empty[STAGES];   // stage consumed (consumer thread 0 arrive)
+  __shared__ TileDesc sdesc[STAGES];
+
+  // stage b: [ids | keys | values] at smem + b * kSet (arithmetic keeps the
+  // shared address space visible to the compiler: LDS, no local arrays)
+  auto stI = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * Cfg::kSet); };
+  auto stK = [&](int b) { return reinterpret_cast<K*>(smem + b * Cfg::kSet + Cfg::kBufI); };
+  auto stV = [&](int b) { return reinterpret_cast<V*>(smem + b * Cfg::kSet + Cfg::kBufI + Cfg::kBufK); };
+  unsigned char* p = smem + STAGES * Cfg::kSet;
+  uint32_t* srtA = reinterpret_cast<uint32_t*>(p); p += T * 4;
+  uint32_t* srtB = reinterpret_cast<uint32_t*>(p); p += T * 4;
+  uint64_t* cursor = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
+  uint64_t* wbase = reinterpret_cast<uint64_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 8);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
+  uint32_t* dh = reinterpret_cast<uint32_t*>(p);
+  uint32_t* pm = dh + kDistWarps * kDhStride;
+  for (int i = threadIdx.x; i < kDistWarps * kDhStride; i += blockDim.x) pm[i] = 0;
+  const int dbg = g_dist_debug;
+  const int w = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < STAGES; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
+
+  // ---- producer warp (lane 0): claims work items, stages tiles ----
+  if (w == kDistWarps) {
+    if (lane == 0) dist_producer<K, V, Cfg>(smem, sk, sv, ids, n_src, work, n_work, ctr, full, empty, sdesc, dbg);
+    return;
+  }
 
   uint32_t nb = 0;
   const bool prof = (dbg & 4) && threadIdx.x == 0;
@@ -286,16 +345,8 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
   };
   for (uint32_t q = 0;; ++q) {
     const int buf = q % STAGES;
-    // keep STAGES tiles in flight (stage q % STAGES was released by the
-    // end-of-tile barrier of tile q - STAGES)
-    if (threadIdx.x == 0) {
-      while (issued < q + STAGES && !pdone) {
-        issue_one(issued % STAGES);
-        ++issued;
-      }
-    }
     mark(9);
-    mbar_wait(&bars[buf], (q / STAGES) & 1);
+    mbar_wait(&full[buf], (q / STAGES) & 1);
     const TileDesc td = sdesc[buf];
     if (td.cnt == 0) break;   // uniform: every thread read the same marker
     const uint64_t begin = td.begin;
@@ -316,7 +367,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
     const K* tK = stK(buf) + pk.sh;
     const V* tV = stV(buf) + pv.sh;
     mark(0);
-    __syncthreads();   // cursors and zeroed histogram visible
+    csync<kDistWarps>();   // cursors and zeroed histogram visible
     mark(1);
 
     // ids -> histogram + (bucket << 12 | index) entries; pass-1 ranks
@@ -333,7 +384,7 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       e[k] = (b << kIdxBits) | i;
     }
     radix_rank<ITEMS, kDistWarps, HW>(e, kIdxBits, dh, pm, rk);
-    __syncthreads();
+    csync<kDistWarps>();
     mark(2);
     // one fused scan: pass-1 digit bases and the histogram (bucket starts)
     const uint32_t per = (nb + kDistThreads - 1) / kDistThreads;
@@ -348,24 +399,24 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
       hist[b] = 0;
       trun += h;
     }
-    __syncthreads();
+    csync<kDistWarps>();
     mark(3);
     radix_scatter<ITEMS>(e, rk, kIdxBits, dh, srtA);
-    __syncthreads();
+    csync<kDistWarps>();
     mark(4);
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) e[k] = srtA[w * (32 * ITEMS) + k * 32 + lane];
     radix_rank<ITEMS, kDistWarps, HW>(e, kIdxBits + kRadixBits, dh, pm, rk);
-    __syncthreads();
+    csync<kDistWarps>();
     mark(5);
     radix_scan<kDistWarps>(dh, red64, 0);
-    __syncthreads();
+    csync<kDistWarps>();
     mark(6);
     radix_scatter<ITEMS>(e, rk, kIdxBits + kRadixBits, dh, srtB);
-    __syncthreads();
+    csync<kDistWarps>();
     mark(7);
     // contiguous per-bucket runs out of the staged tile
-    if (pk.ok && (!kHasV || pv.ok) && !dbg) {
+    if (pk.ok && (!kHasV || pv.ok) && !(dbg & 3)) {
       // batches of loads first (no branches between them), then the stores
       constexpr int kB = ITEMS >= 4 ? 4 : ITEMS;
 #pragma unroll
@@ -408,7 +459,8 @@ k_distribute(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t*
         }
       }
     }
-    __syncthreads();   // stage `buf` may be refilled; wbase / srtB / sdesc reusable
+    csync<kDistWarps>();   // stage `buf` may be refilled; wbase / srtB / sdesc reusable
+    if (threadIdx.x == 0) mbar_arrive(&empty[buf]);
     mark(8);
   }
   if (prof) {

@@ -1,0 +1,307 @@
+// Single-pass blocked distributing (core.py:321-380, aggregate.py:172-193):
+// the fast path of the stable scatter when its tables fit shared memory and
+// every node's output range is below 2^32 records.
+//
+// Same pipeline as dist.cuh (persistent CTAs, a producer warp staging
+// 4096-record tiles of [ids | keys | values] by TMA, dynamic claiming of
+// work items), but each tile is ordered by bucket in ONE counting pass
+// instead of two 7-bit LSD passes:
+//   A. every warp walks its 256 records in index order; a shared atomicAdd
+//      on the warp's private u16 counter of the record's bucket (two
+//      buckets packed per word, +1 / +65536) returns the record's rank
+//      among the warp's earlier records of that bucket -- in lane order
+//      within one instruction on sm_100 (probe.cuh checks it at load time;
+//      without it dist.cuh's kernel runs instead);
+//   B. per bucket, an exclusive scan over the warps' counters plus one
+//      CTA scan of the bucket totals turn counters into tile positions
+//      (bucket start + earlier warps), and advance the row cursors;
+//   C. records scatter their (bucket, index) into the sorted order;
+//   D. threads write sorted positions, so lanes emit contiguous per-bucket
+//      runs, and re-zero their counters.
+// Positions are row-relative u32 (X[row][0] + offset): 5 barriers per
+// tile instead of 9, and the counters replace the radix buffers.
+#pragma once
+
+#include "dist.cuh"
+
+namespace ss {
+
+template <typename K, typename V, int TILE, int NT, int STAGES>
+struct Dist1Cfg : DistCfg<K, V, TILE, NT, STAGES> {
+  using Base = DistCfg<K, V, TILE, NT, STAGES>;
+  static constexpr int kWarps = NT / 32;
+  // u16 counter pairs per warp row: ceil(nb / 2) rounded up to even (uint2 loads)
+  __host__ __device__ static uint32_t pair_stride(uint32_t stride) { return ((stride + 1) / 2 + 1) & ~1u; }
+  static size_t smem_bytes(uint32_t stride) {
+    return STAGES * Base::kSet + static_cast<size_t>(TILE) * 4 + 2 * Base::up16(static_cast<size_t>(stride) * 4) +
+           static_cast<size_t>(kWarps) * pair_stride(stride) * 4 + 64;
+  }
+};
+
+template <typename K, typename V, int TILE, int NT, int STAGES>
+__global__ void __launch_bounds__(NT + 32, 1)   // 17 warps: one sub-partition holds 5 -> <= 96 registers
+
+k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
+              K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
+              const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
+              uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr) {
+  using Cfg = Dist1Cfg<K, V, TILE, NT, STAGES>;
+  constexpr int NW = NT / 32;
+  constexpr bool kHasV = Cfg::kValBytes > 0;
+  constexpr int T = TILE;
+  constexpr int ITEMS = T / NT;
+  static_assert(T <= 4096 && ITEMS * NT == T, "tile index is 12 bits");
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long red64[33];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t empty[STAGES];
+  __shared__ TileDesc sdesc[STAGES];
+
+  auto stI = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * Cfg::kSet); };
+  auto stK = [&](int b) { return reinterpret_cast<K*>(smem + b * Cfg::kSet + Cfg::kBufI); };
+  auto stV = [&](int b) { return reinterpret_cast<V*>(smem + b * Cfg::kSet + Cfg::kBufI + Cfg::kBufK); };
+  const uint32_t pstride = Cfg::pair_stride(stride);
+  unsigned char* p = smem + STAGES * Cfg::kSet;
+  uint32_t* srt = reinterpret_cast<uint32_t*>(p); p += T * 4;
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
+  uint32_t* cntw = reinterpret_cast<uint32_t*>(p);   // [NW][pstride] u16 pairs
+  for (uint32_t i = threadIdx.x; i < NW * pstride; i += blockDim.x) cntw[i] = 0;
+  const int dbg = g_dist_debug;
+  const int w = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < STAGES; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (w == NW) {
+    if (lane == 0) dist_producer<K, V, Cfg>(smem, sk, sv, ids, n_src, work, n_work, ctr, full, empty, sdesc, dbg);
+    return;
+  }
+
+  uint32_t nb = 0, npairs = 0;
+  uint64_t rbase = 0;   // X[row][0]: positions below are relative to it
+  uint32_t* mine = cntw + w * pstride;
+  const bool prof = (dbg & 4) && threadIdx.x == 0;
+  unsigned long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tlast = prof ? clock64() : 0;
+  auto mark = [&](int ph) {
+    if (prof) {
+      const unsigned long long t = clock64();
+      pacc[ph] += t - tlast;
+      tlast = t;
+    }
+  };
+  for (uint32_t q = 0;; ++q) {
+    const int buf = q % STAGES;
+    mbar_wait(&full[buf], (q / STAGES) & 1);
+    const TileDesc td = sdesc[buf];
+    if (td.cnt == 0) break;
+    const uint64_t begin = td.begin;
+    const uint32_t cnt = td.cnt;
+    if (td.fresh) {   // new work item: its X row (row-relative) and bucket count
+      nb = fixed_nb ? fixed_nb : n_light + nodes[td.node].n_heavy;
+      if (nb > keep_below) nb = keep_below;
+      npairs = (nb + 1) >> 1;
+      const uint64_t* xrow = X + td.row * stride;
+      rbase = xrow[0];   // bucket-major layout: bucket 0's cursor is the row minimum
+      for (uint32_t b = threadIdx.x; b < nb; b += NT) cursor[b] = static_cast<uint32_t>(xrow[b] - rbase);
+    }
+    const Bulk16<uint16_t> pi(ids, n_src, begin, cnt);
+    const Bulk16<K> pk(sk, n_src, begin, cnt);
+    const Bulk16<V> pv(sv, n_src, begin, cnt);
+    const uint16_t* tI = stI(buf) + pi.sh;
+    const K* tK = stK(buf) + pk.sh;
+    const V* tV = stV(buf) + pv.sh;
+    mark(0);
+
+    // A. in-warp ranks: old value of the warp's packed counter
+    uint32_t bk[ITEMS], rk[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
+      uint32_t b = kSentinel;
+      if (i < cnt) {
+        b = pi.ok ? tI[i] : ids[begin + i];
+        if (b >= nb) b = kSentinel;
+      }
+      bk[k] = b;
+      rk[k] = 0;
+      if (b != kSentinel) {
+        const uint32_t sh = (b & 1u) << 4;
+        rk[k] = (atomicAdd(&mine[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
+      }
+      __syncwarp();   // item k's increments precede item k+1's
+    }
+    csync<NW>();
+    mark(2);
+
+    // B. per bucket pair: exclusive scan over warps, then over buckets.
+    //    Thread t owns pairs 2t, 2t+1 (one uint2 per warp row);
+    //    thread-contiguous pairs keep the CTA scan in bucket order.
+    uint32_t n_valid;
+    if (npairs <= 2 * NT) {
+      const uint32_t j0 = 2 * threadIdx.x;
+      const bool own = j0 < npairs;
+      uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+#pragma unroll
+      for (int v = 0; v < NW; ++v) {
+        const uint2 c = own ? *reinterpret_cast<const uint2*>(cntw + v * pstride + j0) : make_uint2(0, 0);
+        l0 += c.x & 0xFFFFu;
+        h0 += c.x >> 16;
+        l1 += c.y & 0xFFFFu;
+        h1 += c.y >> 16;
+      }
+      unsigned long long total64;
+      const uint32_t s0 = static_cast<uint32_t>(cscan_u64<NW>(l0 + h0 + l1 + h1, red64, total64));
+      n_valid = static_cast<uint32_t>(total64);
+      if (own) {
+        // bucket starts: 2j0, 2j0+1, 2j0+2, 2j0+3
+        uint32_t a0 = s0, a1 = s0 + l0, a2 = s0 + l0 + h0, a3 = s0 + l0 + h0 + l1;
+        const uint32_t b0 = 2 * j0;
+        wbase[b0] = cursor[b0] - a0;   // modular: cursor + (s - start) below
+        cursor[b0] += l0;
+        if (b0 + 1 < nb) {
+          wbase[b0 + 1] = cursor[b0 + 1] - a1;
+          cursor[b0 + 1] += h0;
+        }
+        if (b0 + 2 < nb) {
+          wbase[b0 + 2] = cursor[b0 + 2] - a2;
+          cursor[b0 + 2] += l1;
+        }
+        if (b0 + 3 < nb) {
+          wbase[b0 + 3] = cursor[b0 + 3] - a3;
+          cursor[b0 + 3] += h1;
+        }
+#pragma unroll
+        for (int v = 0; v < NW; ++v) {   // tile position of warp v's first record per bucket
+          uint2* cp = reinterpret_cast<uint2*>(cntw + v * pstride + j0);
+          const uint2 c = *cp;
+          *cp = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
+          a0 += c.x & 0xFFFFu;
+          a1 += c.x >> 16;
+          a2 += c.y & 0xFFFFu;
+          a3 += c.y >> 16;
+        }
+      }
+    } else {   // many buckets: contiguous chunks of pairs, counters re-read
+      const uint32_t per = (npairs + NT - 1) / NT;
+      const uint32_t j0 = min(npairs, threadIdx.x * per), j1 = min(npairs, j0 + per);
+      uint32_t tot_local = 0;
+      for (uint32_t j = j0; j < j1; ++j)
+#pragma unroll
+        for (int v = 0; v < NW; ++v) {
+          const uint32_t cv = cntw[v * pstride + j];
+          tot_local += (cv & 0xFFFFu) + (cv >> 16);
+        }
+      unsigned long long total64;
+      uint32_t run = static_cast<uint32_t>(cscan_u64<NW>(tot_local, red64, total64));
+      n_valid = static_cast<uint32_t>(total64);
+      for (uint32_t j = j0; j < j1; ++j) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int v = 0; v < NW; ++v) {
+          const uint32_t cv = cntw[v * pstride + j];
+          lo += cv & 0xFFFFu;
+          hi += cv >> 16;
+        }
+        uint32_t alo = run, ahi = run + lo;
+        const uint32_t b0 = 2 * j;
+        wbase[b0] = cursor[b0] - alo;
+        cursor[b0] += lo;
+        if (b0 + 1 < nb) {
+          wbase[b0 + 1] = cursor[b0 + 1] - ahi;
+          cursor[b0 + 1] += hi;
+        }
+#pragma unroll
+        for (int v = 0; v < NW; ++v) {
+          const uint32_t cv = cntw[v * pstride + j];
+          cntw[v * pstride + j] = alo | (ahi << 16);
+          alo += cv & 0xFFFFu;
+          ahi += cv >> 16;
+        }
+        run += lo + hi;
+      }
+    }
+    csync<NW>();
+    mark(3);
+
+    // C. scatter (bucket << 12 | index) into the sorted order
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t b = bk[k];
+      if (b == kSentinel) continue;
+      const uint32_t sh = (b & 1u) << 4;
+      const uint32_t s = ((mine[b >> 1] >> sh) & 0xFFFFu) + rk[k];
+      srt[s] = (b << kIdxBits) | (w * (32 * ITEMS) + k * 32 + lane);
+    }
+    csync<NW>();
+    mark(4);
+
+    // D. sorted write-out (contiguous per-bucket runs); re-zero counters
+    if (npairs <= 2 * NT) {
+      const uint32_t j0 = 2 * threadIdx.x;
+      if (j0 < npairs)
+#pragma unroll
+        for (int v = 0; v < NW; ++v) *reinterpret_cast<uint2*>(cntw + v * pstride + j0) = make_uint2(0, 0);
+    } else {
+      for (uint32_t j = threadIdx.x; j < npairs; j += NT)
+#pragma unroll
+        for (int v = 0; v < NW; ++v) cntw[v * pstride + j] = 0;
+    }
+    if (pk.ok && (!kHasV || pv.ok) && !(dbg & 3)) {
+      constexpr int kB = ITEMS >= 4 ? 4 : ITEMS;
+#pragma unroll
+      for (int k0 = 0; k0 < ITEMS; k0 += kB) {
+        uint64_t dd[kB];
+        K kk[kB];
+        V vv[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const uint32_t s = threadIdx.x + (k0 + k) * NT;
+          ok[k] = s < n_valid;
+          const uint32_t ent = ok[k] ? srt[s] : 0u;   // srt beyond n_valid is stale
+          const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
+          dd[k] = rbase + static_cast<uint32_t>(wbase[b] + s);
+          kk[k] = tK[i];
+          if constexpr (kHasV) vv[k] = tV[i];
+        }
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          if (ok[k]) {
+            dk[dd[k]] = kk[k];
+            if constexpr (kHasV) dv[dd[k]] = vv[k];
+          }
+        }
+      }
+    } else {
+      for (uint32_t s = threadIdx.x; s < n_valid; s += NT) {
+        const uint32_t ent = srt[s];
+        const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
+        uint64_t d = rbase + static_cast<uint32_t>(wbase[b] + s);
+        if (dbg & 2) d = begin + s;
+        if (!(dbg & 1)) {
+          dk[d] = pk.ok ? tK[i] : sk[begin + i];
+          if constexpr (kHasV) dv[d] = pv.ok ? tV[i] : sv[begin + i];
+        }
+      }
+    }
+    csync<NW>();   // stage, srt, wbase and sdesc reusable; counters zero
+    if (threadIdx.x == 0) mbar_arrive(&empty[buf]);
+    mark(8);
+  }
+  if (prof) {
+    unsigned long long tot = 0;
+    for (int p = 0; p < 10; ++p) {
+      atomicAdd(&g_dist_prof[p], pacc[p]);
+      tot += pacc[p];
+    }
+    atomicAdd(&g_dist_prof[10], 1ull);
+    atomicMax(&g_dist_prof[11], tot);
+  }
+}
+
+}  // namespace ss

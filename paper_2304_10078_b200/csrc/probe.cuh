@@ -1,7 +1,8 @@
-// Load-time probe of the hardware rank property the distribute kernel's fast
-// path relies on (dist.cuh radix_rank<HW = true>): a shared atomicAdd of 1
-// returns, to the lanes of one warp instruction that hit the same counter,
-// consecutive old values in lane order.  The probe compares those values
+// Load-time probe of the hardware rank property the distribute kernels' fast
+// paths rely on (dist.cuh radix_rank<HW = true>, dist1.cuh): a shared
+// atomicAdd returns, to the lanes of one warp instruction that hit the same
+// counter, old values accumulated in lane order -- for +1 counters and for
+// u16 pairs packed in one word (+1 / +65536).  The probe compares those values
 // with ranks from __match_any_sync on random and skewed digits; any
 // mismatch (or SS_HW_RANK=0) selects the atomicOr-mask path instead.
 #pragma once
@@ -33,12 +34,23 @@ static __global__ void __launch_bounds__(512) k_probe_hw_rank(unsigned long long
     const uint32_t d = on_hot ? static_cast<uint32_t>(x & 3) * 37u : static_cast<uint32_t>(x >> 40) % kProbeBins;
     const bool active = ((x >> 20) & 7) != 0;
     const uint32_t peers = __match_any_sync(0xffffffffu, active ? d : 0x10000u + lane);
-    const uint32_t before = cnt[w][d];
+    // +1 counters (radix_rank) and u16 pairs packed in one word (+1 low /
+    // +65536 high, dist1.cuh) must both hand out lane-ordered old values
+    const bool packed = (it & 1) != 0;
+    uint32_t* word = packed ? &cnt[w][d >> 1] : &cnt[w][d];
+    const uint32_t sh = packed ? 16u * (d & 1u) : 0u;
+    const uint32_t before = *word;
     __syncwarp();
     uint32_t old = 0;
-    if (active) old = atomicAdd(&cnt[w][d], 1u);
+    if (active) old = atomicAdd(word, 1u << sh);
     __syncwarp();
-    if (active && old != before + __popc(peers & lt)) ++nbad;
+    const uint32_t got = packed ? (old >> sh) & 0xFFFFu : old;
+    const uint32_t want = (packed ? (before >> sh) & 0xFFFFu : before) + __popc(peers & lt);
+    if (active && got != want) ++nbad;
+    __syncwarp();
+    if (packed && lane == 0) {   // keep packed halves far from overflow
+      for (int i = 0; i < kProbeBins; ++i) cnt[w][i] &= 0x00FF00FFu;
+    }
     __syncwarp();
   }
   if (nbad) atomicAdd(bad, static_cast<unsigned long long>(nbad));

@@ -18,6 +18,7 @@
 #include "engine.cuh"
 #include "leaf.cuh"
 #include "leaf_warp.cuh"
+#include "dist1.cuh"
 #include "multisplit.cuh"
 #include "probe.cuh"
 #include "sample.cuh"
@@ -44,12 +45,33 @@ inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, u
   auto kern = k_distribute<K, V, TILE, NT, STAGES, HW>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
   int per_sm = 0;
-  SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, dsm));
+  SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 32, dsm));
   const uint32_t grid = std::min<uint32_t>(nwork, 148u * static_cast<uint32_t>(std::max(per_sm, 1)));
   SS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
-  kern<<<grid, NT, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
+  kern<<<grid, NT + 32, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light,
                               fixed_nb, ctr);
   check_launch();
+}
+
+template <typename K, typename V, int TILE>
+inline void launch_distribute1_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
+                                 const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
+                                 uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
+                                 cudaStream_t st, uint32_t* ctr) {
+  const size_t dsm = Dist1Cfg<K, V, TILE, 512, 2>::smem_bytes(stride);
+  auto kern = k_distribute1<K, V, TILE, 512, 2>;
+  SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
+  const uint32_t grid = std::min<uint32_t>(nwork, 148u);
+  SS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
+  kern<<<grid, 512 + 32, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
+                                    n_light, fixed_nb, ctr);
+  check_launch();
+}
+
+// Which distribute kernel (SS_DIST_KERNEL=radix forces dist.cuh's; tests use it).
+inline bool dist_radix_forced() {
+  const char* e = std::getenv("SS_DIST_KERNEL");
+  return e && std::strcmp(e, "radix") == 0;
 }
 
 // Distribute launch shapes (SS_DIST_SHAPE, measurement knob):
@@ -86,7 +108,19 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light, fixed_nb, st, ctr
   constexpr size_t kHalfSm = (228 * 1024) / 2 - 2048;   // two CTAs per SM
   const int shape = dist_shape();
-  if (hw_rank_ok()) {
+  // single pass: hardware-ordered ranks, row-relative u32 positions, tables fit
+  bool done = false;
+  if (hw_rank_ok() && !dist_radix_forced() && n_src <= 0xFFFFFFFFull) {
+    if (Dist1Cfg<K, V, 4096, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) {
+      launch_distribute1_t<K, V, 4096>(SS_DIST_ARGS);
+      done = true;
+    } else if (Dist1Cfg<K, V, 2048, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) {
+      launch_distribute1_t<K, V, 2048>(SS_DIST_ARGS);
+      done = true;
+    }
+  }
+  if (done) {
+  } else if (hw_rank_ok()) {
     if (shape == 1 && DistCfg<K, V, 2048, 256, 1>::smem_bytes(stride) <= kHalfSm) {
       launch_distribute_t<K, V, 2048, 256, 1, true>(SS_DIST_ARGS);
     } else {

@@ -389,7 +389,7 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       auto kern = k_distribute<K, V, kTile, 512, 2, false>;
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
       SS_CUDA(cudaMemsetAsync(pp.d_ctr, 0, sizeof(uint32_t), st));
-      kern<<<std::min<uint32_t>(nw, 148), 512, dsm, st>>>(
+      kern<<<std::min<uint32_t>(nw, 148), 512 + 32, dsm, st>>>(   // + producer warp
           static_cast<const K*>(keys), static_cast<const V*>(values), pp.d_ids, n, static_cast<K*>(dst_keys),
           static_cast<V*>(dst_values), pp.d_work, nw, pp.d_node, pp.d_X, pp.stride, 0xFFFFFFFFu, 0, parts,
           pp.d_ctr);
