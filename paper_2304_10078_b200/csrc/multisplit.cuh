@@ -81,7 +81,7 @@ __device__ __forceinline__ void count_add(uint32_t* cnt, uint32_t b, bool valid,
 }
 
 template <typename K, typename BF>
-__global__ void __launch_bounds__(kCountThreads)
+__global__ void __launch_bounds__(kCountThreads, 6)
 k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_work,
         const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, BF bf,
         uint16_t* __restrict__ ids_out) {
@@ -98,12 +98,28 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
     __syncthreads();
     const uint64_t begin = wk.begin;
     const uint32_t len = wk.len;
-    for (uint32_t base = 0; base < len; base += kCountThreads * kCountItems) {
+    const K* ws = src + begin;                                   // 32-bit offsets below
+    uint16_t* wids = ids_out ? ids_out + begin : nullptr;
+    constexpr uint32_t kBatch = kCountThreads * kCountItems;
+    const uint32_t full = len - len % kBatch;
+    for (uint32_t base = 0; base < full; base += kBatch) {      // no bounds checks
+      K keys[kCountItems];
+#pragma unroll
+      for (int k = 0; k < kCountItems; ++k) keys[k] = __ldg(ws + base + k * kCountThreads + threadIdx.x);
+#pragma unroll
+      for (int k = 0; k < kCountItems; ++k) {
+        const uint32_t i = base + k * kCountThreads + threadIdx.x;
+        const uint32_t b = bf(keys[k], begin + i);
+        atomicAdd(&cnt[b], 1u);
+        if (wids) wids[i] = static_cast<uint16_t>(b);           // consumed by k_distribute
+      }
+    }
+    for (uint32_t base = full; base < len; base += kBatch) {    // tail
       K keys[kCountItems];
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
-        keys[k] = i < len ? ldg_key(src, begin + i) : K(0);
+        keys[k] = i < len ? __ldg(ws + i) : K(0);
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
@@ -111,7 +127,7 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
         const bool valid = i < len;
         const uint32_t b = valid ? bf(keys[k], begin + i) : 0u;
         count_add(cnt, b, valid, hot, hot_bits);
-        if (ids_out && valid) ids_out[begin + i] = static_cast<uint16_t>(b);   // consumed by k_distribute
+        if (wids && valid) wids[i] = static_cast<uint16_t>(b);
       }
     }
     __syncthreads();
@@ -234,7 +250,16 @@ __device__ __forceinline__ void copy_span(T* __restrict__ dst, const T* __restri
     const uint64_t v0 = lo + head, nv = (hi - v0) / per;
     const uint4* s4 = reinterpret_cast<const uint4*>(src + v0);
     uint4* d4 = reinterpret_cast<uint4*>(dst + v0);
-    for (uint64_t i = tid; i < nv; i += nthreads) d4[i] = s4[i];
+    uint64_t i = tid;
+    for (; i + 3 * nthreads < nv; i += 4 * nthreads) {   // 4 loads in flight per thread
+      const uint4 x0 = __ldcs(s4 + i), x1 = __ldcs(s4 + i + nthreads), x2 = __ldcs(s4 + i + 2 * nthreads),
+                  x3 = __ldcs(s4 + i + 3 * nthreads);
+      d4[i] = x0;
+      d4[i + nthreads] = x1;
+      d4[i + 2 * nthreads] = x2;
+      d4[i + 3 * nthreads] = x3;
+    }
+    for (; i < nv; i += nthreads) d4[i] = s4[i];
     for (uint64_t i = v0 + nv * per + tid; i < hi; i += nthreads) dst[i] = src[i];
   } else {
     for (uint64_t i = lo + tid; i < hi; i += nthreads) dst[i] = src[i];

@@ -31,6 +31,8 @@ constexpr uint32_t kSampleGridMax = 148;
 constexpr uint32_t kLeafGlobalGridMax = 296;
 constexpr size_t kSampleSmem = kSampleSmemCap * 4;
 constexpr int kDistShapeDefault = 0;
+constexpr uint64_t kCopySnapNodes = 4096;   // nodes whose heavy copy-back can run on the side stream
+constexpr uint32_t kCopySideCtas = 64;
 
 inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
   return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
@@ -197,6 +199,13 @@ struct SortEngine {
   V* S_v = nullptr;
   Node* d_nodes = nullptr;
   Node* d_next = nullptr;
+  Node* d_nodes_cp = nullptr;    // snapshot for the side-stream heavy copy
+  uint64_t* d_off_cp = nullptr;
+  // side stream: heavy copy-back overlapped with the following levels
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool side_busy = false;
+  uint64_t snap_nodes = 0;
   uint64_t* d_heavy = nullptr;
   Work* d_work = nullptr;
   uint32_t* d_grp_node = nullptr;
@@ -240,6 +249,9 @@ struct SortEngine {
     d_X = a.take<uint64_t>(max_rows * stride);
     d_P = a.take<uint64_t>(max_grps * stride);
     d_off = a.take<uint64_t>(max_nodes * (stride + 1));
+    snap_nodes = std::min<uint64_t>(max_nodes, kCopySnapNodes);
+    d_nodes_cp = a.take<Node>(snap_nodes);
+    d_off_cp = a.take<uint64_t>(snap_nodes * (stride + 1));
     d_ccnt = a.take<uint32_t>(max_nodes * 4);
     d_misc = a.take<uint64_t>(8);
     d_ctr = a.take<uint32_t>(4);
@@ -430,14 +442,38 @@ struct SortEngine {
     check_launch();
     tr.launched();
 
-    // heavy buckets are final: copy them back when they landed in S
-    if (from_a) {
+    // heavy buckets are final: copy them back when they landed in S.  The
+    // copy touches only heavy ranges; every later step of the sort works on
+    // light ranges (disjoint), so it runs on a side stream, overlapped with
+    // the next level, from a snapshot of this level's nodes and offsets.
+    if (from_a && nn > snap_nodes) {   // wide level: copy in order on the main stream
       tr.begin(kPhCopy);
       const uint32_t gy = std::min<uint32_t>(nn, 65535);
       const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(1184, gy))));
       k_copy_heavy<K, V><<<dim3(gx, gy), 256, 0, st>>>(S_k, S_v, A_k, A_v, d_nodes, nn, d_off, stride,
                                                       P.light_buckets);
       check_launch();
+      tr.launched();
+    } else if (from_a) {
+      tr.begin(kPhCopy);
+      if (side_busy) SS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));   // snapshot buffers free
+      SS_CUDA(cudaMemcpyAsync(d_nodes_cp, d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToDevice, st));
+      SS_CUDA(cudaMemcpyAsync(d_off_cp, d_off, nn * (stride + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      SS_CUDA(cudaEventRecord(ev_fork, st));
+      SS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+      // few CTAs (bandwidth needs ~1/3 of the SMs): the next level's kernels
+      // keep the rest of the GPU
+      static const uint32_t side_ctas = [] {
+        const char* e = std::getenv("SS_COPY_CTAS");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : kCopySideCtas;
+      }();
+      const uint32_t gy = std::min<uint32_t>(nn, side_ctas);
+      const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, side_ctas / gy));
+      k_copy_heavy<K, V><<<dim3(gx, gy), 512, 0, side>>>(S_k, S_v, A_k, A_v, d_nodes_cp, nn, d_off_cp, stride,
+                                                        P.light_buckets);
+      check_launch();
+      SS_CUDA(cudaEventRecord(ev_join, side));
+      side_busy = true;
       tr.launched();
     }
 
@@ -509,6 +545,23 @@ struct SortEngine {
   }
 
   void run(Tracker& tr) {
+    SS_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    SS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    SS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    struct Join {   // the caller's stream waits for the side stream on every exit
+      SortEngine* e;
+      ~Join() {
+        if (e->side_busy) cudaStreamWaitEvent(e->st, e->ev_join, 0);
+        cudaEventDestroy(e->ev_fork);
+        cudaEventDestroy(e->ev_join);
+        cudaStreamDestroy(e->side);   // released once its work completes
+        e->side_busy = false;
+      }
+    } join{this};
+    run_levels(tr);
+  }
+
+  void run_levels(Tracker& tr) {
     if (tel) tel->scratch_allocations += 1;   // one scratch per call (core.py:591-592)
     if (tel) {
       tel->nodes += 1;
