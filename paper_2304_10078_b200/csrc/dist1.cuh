@@ -20,6 +20,8 @@
 //      runs, and re-zero their counters.
 // Positions are row-relative u32 (X[row][0] + offset): 5 barriers per
 // tile instead of 9, and the counters replace the radix buffers.
+// key_below: keys of buckets >= key_below are not written (semisort's heavy
+// buckets hold one key; the copy-back fills it, k_copy_heavy_fill).
 #pragma once
 
 #include "dist.cuh"
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(NT + 32, 1)   // 17 warps: one sub-partition h
 k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
               K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
               const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
-              uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr) {
+              uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr, uint32_t key_below) {
   using Cfg = Dist1Cfg<K, V, TILE, NT, STAGES>;
   constexpr int NW = NT / 32;
   constexpr bool kHasV = Cfg::kValBytes > 0;
@@ -258,22 +260,23 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
         uint64_t dd[kB];
         K kk[kB];
         V vv[kB];
-        bool ok[kB];
+        bool ok[kB], wk[kB];
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
           const uint32_t s = threadIdx.x + (k0 + k) * NT;
           ok[k] = s < n_valid;
           const uint32_t ent = ok[k] ? srt[s] : 0u;   // srt beyond n_valid is stale
           const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
+          wk[k] = ok[k] && b < key_below;
           dd[k] = rbase + static_cast<uint32_t>(wbase[b] + s);
           kk[k] = tK[i];
           if constexpr (kHasV) vv[k] = tV[i];
         }
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
-          if (ok[k]) {
-            dk[dd[k]] = kk[k];
-            if constexpr (kHasV) dv[dd[k]] = vv[k];
+          if (wk[k]) dk[dd[k]] = kk[k];
+          if constexpr (kHasV) {
+            if (ok[k]) dv[dd[k]] = vv[k];
           }
         }
       }
@@ -284,7 +287,7 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
         uint64_t d = rbase + static_cast<uint32_t>(wbase[b] + s);
         if (dbg & 2) d = begin + s;
         if (!(dbg & 1)) {
-          dk[d] = pk.ok ? tK[i] : sk[begin + i];
+          if (b < key_below) dk[d] = pk.ok ? tK[i] : sk[begin + i];
           if constexpr (kHasV) dv[d] = pv.ok ? tV[i] : sv[begin + i];
         }
       }

@@ -282,6 +282,66 @@ __global__ void k_copy_heavy(const K* __restrict__ sk, const V* __restrict__ sv,
   }
 }
 
+// Heavy copy-back with key fill (semisort=): a heavy bucket holds a single
+// key, so the distribute skipped its keys (key_below) and only the values
+// move S -> A; the keys are filled from the node's heavy table.  off[j] are
+// node-relative bucket offsets ([n_light + t] = start of heavy bucket t,
+// [n_light + n_heavy] = node size); heavy[j * mh + t] its key.
+constexpr uint64_t kFillChunk = 1 << 16;
+
+template <typename K>
+__device__ __forceinline__ void fill_span(K* __restrict__ dst, uint64_t lo, uint64_t hi, K key) {
+  if (hi <= lo) return;
+  constexpr uint64_t per = 16 / sizeof(K);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst + lo);
+  uint64_t head = ((16 - (a & 15)) & 15) / sizeof(K);
+  if (head > hi - lo) head = hi - lo;
+  for (uint64_t i = lo + threadIdx.x; i < lo + head; i += blockDim.x) dst[i] = key;
+  const uint64_t v0 = lo + head, nv = (hi - v0) / per;
+  uint4 pat;
+  K* pk = reinterpret_cast<K*>(&pat);
+#pragma unroll
+  for (uint64_t q = 0; q < per; ++q) pk[q] = key;
+  uint4* d4 = reinterpret_cast<uint4*>(dst + v0);
+  for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) d4[i] = pat;
+  for (uint64_t i = v0 + nv * per + threadIdx.x; i < hi; i += blockDim.x) dst[i] = key;
+}
+
+template <typename K, typename V>
+__global__ void k_copy_heavy_fill(K* __restrict__ dk, const V* __restrict__ sv, V* __restrict__ dv,
+                                  const Node* __restrict__ nodes, uint32_t n_nodes, const uint64_t* __restrict__ off,
+                                  uint32_t stride, uint32_t n_light, const uint64_t* __restrict__ heavy, uint32_t mh) {
+  constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  __shared__ uint32_t s_t0;
+  for (uint32_t j = blockIdx.y; j < n_nodes; j += gridDim.y) {
+    const Node nd = nodes[j];
+    const uint64_t* o = off + static_cast<uint64_t>(j) * (stride + 1) + n_light;   // o[t]: heavy bucket t
+    const uint64_t h0 = o[0], h1 = nd.size;
+    if (kHasV) {
+      const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+      copy_span(dv, sv, nd.lo + h0, nd.lo + h1, tid, static_cast<uint64_t>(gridDim.x) * blockDim.x);
+    }
+    for (uint64_t c0 = h0 + blockIdx.x * kFillChunk; c0 < h1; c0 += gridDim.x * kFillChunk) {
+      const uint64_t c1 = min(h1, c0 + kFillChunk);
+      if (threadIdx.x == 0) {   // last bucket starting at or before c0
+        uint32_t lo = 0, hi = nd.n_heavy;   // o[lo] <= c0 < o[hi]
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (o[mid] <= c0) lo = mid;
+          else hi = mid;
+        }
+        s_t0 = lo;
+      }
+      __syncthreads();
+      for (uint32_t t = s_t0; t < nd.n_heavy && o[t] < c1; ++t) {
+        const uint64_t b0 = max(c0, o[t]), b1 = min(c1, o[t + 1]);
+        fill_span(dk, nd.lo + b0, nd.lo + b1, static_cast<K>(heavy[static_cast<uint64_t>(j) * mh + t]));
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <typename K, typename V>
 __global__ void k_copy_range(const K* __restrict__ sk, const V* __restrict__ sv, K* __restrict__ dk,
                              V* __restrict__ dv, uint64_t lo, uint64_t hi) {

@@ -59,14 +59,14 @@ template <typename K, typename V, int TILE>
 inline void launch_distribute1_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
                                  const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
                                  uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
-                                 cudaStream_t st, uint32_t* ctr) {
+                                 cudaStream_t st, uint32_t* ctr, uint32_t key_below) {
   const size_t dsm = Dist1Cfg<K, V, TILE, 512, 2>::smem_bytes(stride);
   auto kern = k_distribute1<K, V, TILE, 512, 2>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
   const uint32_t grid = std::min<uint32_t>(nwork, 148u);
   SS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
   kern<<<grid, 512 + 32, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
-                                    n_light, fixed_nb, ctr);
+                                    n_light, fixed_nb, ctr, key_below);
   check_launch();
 }
 
@@ -96,7 +96,7 @@ template <typename K, typename V>
 inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
                               uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
                               uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st,
-                              uint64_t n_src, uint32_t* ctr) {
+                              uint64_t n_src, uint32_t* ctr, uint32_t key_below = 0xFFFFFFFFu) {
   if (!nwork) return;
   static const int dbg = [] {
     const char* e = std::getenv("SS_DIST_DEBUG");
@@ -114,10 +114,10 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   bool done = false;
   if (hw_rank_ok() && !dist_radix_forced() && n_src <= 0xFFFFFFFFull) {
     if (Dist1Cfg<K, V, 4096, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) {
-      launch_distribute1_t<K, V, 4096>(SS_DIST_ARGS);
+      launch_distribute1_t<K, V, 4096>(SS_DIST_ARGS, key_below);
       done = true;
     } else if (Dist1Cfg<K, V, 2048, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) {
-      launch_distribute1_t<K, V, 2048>(SS_DIST_ARGS);
+      launch_distribute1_t<K, V, 2048>(SS_DIST_ARGS, key_below);
       done = true;
     }
   }
@@ -201,6 +201,7 @@ struct SortEngine {
   Node* d_next = nullptr;
   Node* d_nodes_cp = nullptr;    // snapshot for the side-stream heavy copy
   uint64_t* d_off_cp = nullptr;
+  uint64_t* d_heavy_cp = nullptr;
   // side stream: heavy copy-back overlapped with the following levels
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -252,6 +253,7 @@ struct SortEngine {
     snap_nodes = std::min<uint64_t>(max_nodes, kCopySnapNodes);
     d_nodes_cp = a.take<Node>(snap_nodes);
     d_off_cp = a.take<uint64_t>(snap_nodes * (stride + 1));
+    d_heavy_cp = a.take<uint64_t>(snap_nodes * std::max<uint32_t>(P.max_heavy, 1));
     d_ccnt = a.take<uint32_t>(max_nodes * 4);
     d_misc = a.take<uint64_t>(8);
     d_ctr = a.take<uint32_t>(4);
@@ -437,8 +439,9 @@ struct SortEngine {
 
     // blocked distributing
     tr.begin(kPhDistribute);
+    // even levels (A -> S, copied back): heavy keys are filled by the copy
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu,
-                            P.light_buckets, 0, st, n, d_ctr);
+                            P.light_buckets, 0, st, n, d_ctr, from_a ? P.light_buckets : 0xFFFFFFFFu);
     check_launch();
     tr.launched();
 
@@ -450,8 +453,8 @@ struct SortEngine {
       tr.begin(kPhCopy);
       const uint32_t gy = std::min<uint32_t>(nn, 65535);
       const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(1184, gy))));
-      k_copy_heavy<K, V><<<dim3(gx, gy), 256, 0, st>>>(S_k, S_v, A_k, A_v, d_nodes, nn, d_off, stride,
-                                                      P.light_buckets);
+      k_copy_heavy_fill<K, V><<<dim3(gx, gy), 256, 0, st>>>(A_k, S_v, A_v, d_nodes, nn, d_off, stride,
+                                                           P.light_buckets, d_heavy, bf.max_heavy);
       check_launch();
       tr.launched();
     } else if (from_a) {
@@ -459,6 +462,7 @@ struct SortEngine {
       if (side_busy) SS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));   // snapshot buffers free
       SS_CUDA(cudaMemcpyAsync(d_nodes_cp, d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToDevice, st));
       SS_CUDA(cudaMemcpyAsync(d_off_cp, d_off, nn * (stride + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      SS_CUDA(cudaMemcpyAsync(d_heavy_cp, d_heavy, nn * bf.max_heavy * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
       SS_CUDA(cudaEventRecord(ev_fork, st));
       SS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
       // few CTAs (bandwidth needs ~1/3 of the SMs): the next level's kernels
@@ -469,8 +473,8 @@ struct SortEngine {
       }();
       const uint32_t gy = std::min<uint32_t>(nn, side_ctas);
       const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, side_ctas / gy));
-      k_copy_heavy<K, V><<<dim3(gx, gy), 512, 0, side>>>(S_k, S_v, A_k, A_v, d_nodes_cp, nn, d_off_cp, stride,
-                                                        P.light_buckets);
+      k_copy_heavy_fill<K, V><<<dim3(gx, gy), 512, 0, side>>>(A_k, S_v, A_v, d_nodes_cp, nn, d_off_cp, stride,
+                                                             P.light_buckets, d_heavy_cp, bf.max_heavy);
       check_launch();
       SS_CUDA(cudaEventRecord(ev_join, side));
       side_busy = true;
