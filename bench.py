@@ -123,6 +123,127 @@ def cpu_baseline(n_sample: int, repeats: int = 1):
                       f"best of {repeats}, {t:.2f} s"}
 
 
+AGG = {   # the aggregation configs (not the headline metric)
+    "c3": {"metric": "collect_reduce sum64 Grecords/s (n=1e9 u64 k/v, exponential 1e-4)", "family": "exponential",
+           "param": 1e-4, "key_bits": 64, "values": "random", "shift": 32, "kind": "sum64", "b_alg": 56.0,
+           "desc": "c3: collect_reduce(summing64), n=1e9, keys floor(Exponential(scale 1e4)) u64, "
+                   "values uniform u64 >> 32"},
+    "c4": {"metric": "histogram Grecords/s (n=1e9 u32, uniform [0,1e7))", "family": "uniform", "param": 1e7,
+           "key_bits": 32, "values": "none", "shift": 0, "kind": "count", "b_alg": 16.12,
+           "desc": "c4: histogram, n=1e9 u32 keys uniform [0, 1e7), no values"},
+}
+
+
+def agg_cpu_baseline(w, n_sample):
+    """The oracle's collect_reduce (reference algorithm, numpy) on a bounded sample."""
+    import numpy as np
+
+    import oracle as O
+    from oracle.datagen import gen_keys_values
+    c = AGG[w]
+    keys, vals = gen_keys_values(c["family"], c["param"], n_sample, c["key_bits"], seed=1)
+    vals = (vals.astype(np.uint64) >> np.uint64(c["shift"])) if c["values"] != "none" else None
+    P = O.OracleParams.derive(n_sample)
+    t0 = time.perf_counter()
+    O.collect_reduce(keys, vals, P, c["kind"])
+    t = time.perf_counter() - t0
+    return {"value": n_sample / t / 1e9, "unit": "Grecords/s", "cores": 1, "kind": "port",
+            "sample": f"{c['desc'].split(',')[0]} on {n_sample} records (same families, seed 1); reference "
+                      f"algorithm restated in numpy (oracle/), single thread, {t:.2f} s"}
+
+
+def agg_main(args):
+    """--workload c3|c4: collect_reduce / histogram on one GPU (same JSON contract)."""
+    import torch
+
+    import paper_2304_10078_b200 as S
+    from paper_2304_10078_b200.datagen import generate_device
+    w = args.workload
+    c = AGG[w]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n = args.n
+    src = generate_device(c["family"], c["param"], n, key_bits=c["key_bits"], seed=1, values=c["values"],
+                          value_shift=c["shift"], device=dev)
+    adp = S.UIntKeyAdapter()
+    spec = S.ReduceSpec.summing64() if c["kind"] == "sum64" else S.ReduceSpec.counting()
+    params = S.TuningParams.for_input(n)
+
+    def one(tel=None):
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        res = S.collect_reduce(src, adp, spec, params, telemetry=tel)
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), res
+
+    for _ in range(args.warmup):
+        one()
+    tel = S.Telemetry(timing=True)
+    times = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            t, res = one(tel)
+            times.append(t)
+    ms = sum(times) / len(times)
+    groups = int(res.key_tensor.numel()) if res.key_tensor is not None else 0
+    value = n / (ms / 1e3) / 1e9
+    peak_gbs, peak_kind = measured_peaks()
+    dist_ms = tel.phase_ms.get("distribute", 0.0) / args.steps
+    rec_b = c["key_bits"] // 8 + (8 if c["values"] != "none" else 0)
+    moved = tel.bucket_assignments / args.steps
+    achieved = (moved * 2 * rec_b) / (dist_ms / 1e3) / 1e9 if dist_ms > 0 else None
+    e2e = None
+    if not args.no_e2e:
+        hk = torch.empty(n, dtype=src.keys.dtype, pin_memory=True)
+        hk.copy_(src.keys)
+        hv = None
+        if src.values is not None:
+            hv = torch.empty(n, dtype=src.values.dtype, pin_memory=True)
+            hv.copy_(src.values)
+        ts = []
+        for i in range(3):
+            torch.cuda.synchronize()
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            data = S.RecordArray(hk, hv)
+            r = S.collect_reduce(data, adp, spec, params)
+            ok = r.key_tensor.to("cpu", non_blocking=True)
+            oa = r.agg_tensor.to("cpu", non_blocking=True)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1))
+            del data, r, ok, oa
+        e_ms = sum(ts) / len(ts)
+        in_b = n * rec_b
+        out_b = groups * (c["key_bits"] // 8 + 8)
+        e2e = {"value": n / (e_ms / 1e3) / 1e9, "unit": "Grecords/s", "h2d_bytes_per_step": in_b,
+               "d2h_bytes_per_step": out_b, "ms_per_step": e_ms,
+               "path": "RecordArray(pinned host tensors) -> collect_reduce -> (keys, aggs) to host"}
+    cpu = None if args.no_cpu else agg_cpu_baseline(w, 1 << 22)
+    line = {"metric": c["metric"], "value": value, "unit": "Grecords/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64" if c["key_bits"] == 64 else "u32",
+            "data": "synthetic (device-generated, seeded)",
+            "config": {"workload": c["desc"], "n_per_gpu": n, "groups": groups,
+                       "params": "TuningParams.for_input(n) (reference defaults, seed 1)",
+                       "l2": "input (>= 4 GB) larger than the 126 MB L2; read-only, not restored"},
+            "roofline": {"bound": "hbm", "kernel": "k_distribute1 (light-only scatter, all levels)",
+                         "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                         "frac": (achieved / peak_gbs) if achieved else None, "traffic": None,
+                         "peak_kind": peak_kind,
+                         "bytes_model": f"{2 * rec_b} B per bucketed record (read + write {rec_b} B)"},
+            "step_roofline": {"bytes_per_record": c["b_alg"], "achieved_gbs": c["b_alg"] * n / (ms / 1e3) / 1e9,
+                              "peak": peak_gbs},
+            "phase_ms_per_step": {k: v / args.steps for k, v in tel.phase_ms.items()},
+            "gpu_launches": tel.kernel_launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+
+
 def reference_arm(args):
     """--impl reference: the CPU oracle port on a bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
@@ -171,10 +292,16 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=1 << 25)
     ap.add_argument("--ref-n", type=int, default=1 << 24)
     ap.add_argument("--validate", action="store_true", help="check the last output (O(n) device checks)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+                    help="c2 (default, the headline semisort); c3 collect_reduce sum64; c4 histogram")
     args = ap.parse_args()
 
     if args.impl == "reference":
         reference_arm(args)
+        return
+    if args.workload != "c2":
+        if int(os.environ.get("RANK", "0")) == 0:
+            agg_main(args)
         return
 
     import torch
@@ -313,7 +440,7 @@ def main():
                        "n_per_gpu": n, "params": "TuningParams.for_input(n) (reference defaults, seed 1)",
                        "l2": "input restored from a pristine copy before each step (16 GB write flushes L2)",
                        "parallelism": f"dp{world}" if world > 1 else "single"},
-            "roofline": {"bound": "hbm", "kernel": "k_distribute (blocked distributing scatter, all levels)",
+            "roofline": {"bound": "hbm", "kernel": "k_distribute1 (single-pass blocked distributing scatter, all levels)",
                          "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                          "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
                          "peak_kind": peak_kind,

@@ -28,12 +28,14 @@ template <> __device__ __forceinline__ uint64_t val_u64<V16>(const V16& v) { ret
 // Counting matrix + per-row heavy partial sums.
 template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kCountThreads)
-k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, const Work* __restrict__ work, uint32_t n_work,
+k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restrict__ work, uint32_t n_work,
             const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, KeyBuckets bf,
             unsigned long long* __restrict__ HS, uint32_t hs_stride, uint16_t* __restrict__ ids_out) {
   extern __shared__ __align__(16) uint32_t cnt[];
   __shared__ HeavySmem tab;
-  __shared__ unsigned long long hsum[kMaxHeavyDevice];
+  // heavy partial sums as native 32-bit atomics: low half, carries out of
+  // it, high half (a 64-bit shared atomicAdd is a CAS spin loop on sm_100)
+  __shared__ uint32_t hlo[kMaxHeavyDevice], hhi[kMaxHeavyDevice], hcy[kMaxHeavyDevice];
   for (uint32_t wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
     const Work wk = work[wi];
     const Node nd = nodes[wk.node];
@@ -41,38 +43,55 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, const Work* __r
     const uint32_t nb = bf.n_buckets();
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
     if (SUM)
-      for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x) hsum[t] = 0;
+      for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x) hlo[t] = hhi[t] = hcy[t] = 0;
     __syncthreads();
     const uint64_t begin = wk.begin;
     const uint32_t len = wk.len;
     const uint32_t nl = bf.n_light;
     for (uint32_t base = 0; base < len; base += kCountThreads * kCountItems) {
       K keys[kCountItems];
+      uint64_t vals[SUM ? kCountItems : 1];
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
         keys[k] = i < len ? ldg_key(src, begin + i) : K(0);
+        if constexpr (SUM) vals[k] = i < len ? val_u64(sv[begin + i]) : 0ull;
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
-        bool valid = i < len;
-        uint32_t act = __ballot_sync(0xffffffffu, valid);
-        (void)act;
-        if (valid) {
+        if (i < len) {
           const uint32_t b = bf(keys[k], begin + i);
           atomicAdd(&cnt[b], 1u);   // shared atomics are ~free on sm_100 (see count_add)
           ids_out[begin + i] = static_cast<uint16_t>(b);
-          if (SUM && b >= nl)
-            atomicAdd(&hsum[b - nl], static_cast<unsigned long long>(val_u64(sv[begin + i])));
+          if constexpr (SUM) {
+            if (b >= nl) {
+              const uint32_t t = b - nl, lo = static_cast<uint32_t>(vals[k]), hi = static_cast<uint32_t>(vals[k] >> 32);
+              const uint32_t old = atomicAdd(&hlo[t], lo);
+              if (old + lo < old) atomicAdd(&hcy[t], 1u);
+              if (hi) atomicAdd(&hhi[t], hi);
+            }
+          }
         }
       }
     }
     __syncthreads();
     uint32_t* row = C + wk.row * stride;
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) row[b] = cnt[b];
+    __shared__ uint32_t kept;
+    if (threadIdx.x == 0) kept = 0;
+    __syncthreads();
+    uint32_t mine = 0;
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+      row[b] = cnt[b];
+      if (b < nl) mine += cnt[b];
+    }
+    if (mine) atomicAdd(&kept, mine);
+    __syncthreads();
+    // no light record in this row: the light-only distribute skips it (len 0)
+    if (threadIdx.x == 0 && kept == 0) work[wi].len = 0;
     if (SUM)
-      for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x) HS[wk.row * hs_stride + t] = hsum[t];
+      for (uint32_t t = threadIdx.x; t < nd.n_heavy; t += blockDim.x)   // wrapping u64
+        HS[wk.row * hs_stride + t] = (static_cast<unsigned long long>(hhi[t] + hcy[t]) << 32) | hlo[t];
     __syncthreads();
   }
 }
@@ -334,16 +353,15 @@ struct AggEngine {
     const uint32_t cnt = static_cast<uint32_t>(count);
     if (smem_ok) {
       const size_t sm = leaf_fold_smem_bytes(sizeof(K), sum() ? ValTraits<V>::bytes : 0);
-      const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148 * 2));
-      if (sum()) {
-        auto kern = k_leaf_fold_smem<K, V, true>;
+      auto launch = [&](auto kern) {
         SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        int per_sm = 0;
+        SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, sm));
+        const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
         kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G);
-      } else {
-        auto kern = k_leaf_fold_smem<K, V, false>;
-        SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G);
-      }
+      };
+      if (sum()) launch(k_leaf_fold_smem<K, V, true>);
+      else launch(k_leaf_fold_smem<K, V, false>);
       if (tel) tel->leaves_smem += count;
     } else {
       const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, grid_cap));

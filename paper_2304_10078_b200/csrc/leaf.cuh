@@ -154,7 +154,7 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
         if (t == kEmpty32) break;
       }
       if (rk[t] == k) {
-        atomicMin(&a.T[s], i);
+        if (i < t) atomicMin(&a.T[s], i);   // T[s] only decreases: skip when already smaller
         break;
       }
       s = (s + 1) & cmask;

@@ -92,7 +92,7 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
           if (t == kEmpty32) break;
         }
         if (ws.keys[t] == key[k]) {
-          atomicMin(&ws.T[s], i);
+          if (i < t) atomicMin(&ws.T[s], i);   // T[s] only decreases: skip when already smaller
           break;
         }
         s = (s + 1) & cmask;
