@@ -205,6 +205,30 @@ int ss_count_distinct(const void* keys, uint64_t n, uint32_t key_bytes, void* wo
                       uint64_t workspace_bytes, uint64_t* out_count, void* stream);
 uint64_t ss_count_distinct_workspace_bytes(uint64_t n);
 
+/* ---- graph applications -------------------------
+ * CSR graphs: offsets u64[n_vertices + 1], targets u32[m] (device).
+ *
+ * ss_graph_transpose replaces graphs.transpose (graphs.py:77-105): every
+ * edge (u, v) becomes (v, u); the (target, source) records are semisorted
+ * with the identity hash and the CSR rebuilt from the runs, so each
+ * transposed adjacency list is in ascending source order.  Outputs:
+ * out_offsets u64[n_vertices + 1], out_targets u32[m].
+ *
+ * ss_csr_from_edges replaces graphs.from_edges (graphs.py:59-71): CSR by
+ * source, adjacency lists in edge input order (the stable semisort by
+ * source).  Inputs sources/targets u32[m] must be < n_vertices (the Python
+ * layer validates, as the reference does, before calling).
+ *
+ * params: TuningParams bound to m (params.py:64-86).  Workspace:
+ * ss_csr_workspace_bytes (the same for both). */
+uint64_t ss_csr_workspace_bytes(uint64_t n_vertices, uint64_t m, const ss_params* params);
+int ss_graph_transpose(uint64_t n_vertices, uint64_t m, const uint64_t* offsets, const uint32_t* targets,
+                       uint64_t* out_offsets, uint32_t* out_targets, const ss_params* params,
+                       void* workspace, uint64_t workspace_bytes, ss_telemetry* telemetry, void* stream);
+int ss_csr_from_edges(uint64_t n_vertices, uint64_t m, const uint32_t* sources, const uint32_t* targets,
+                      uint64_t* out_offsets, uint32_t* out_targets, const ss_params* params,
+                      void* workspace, uint64_t workspace_bytes, ss_telemetry* telemetry, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

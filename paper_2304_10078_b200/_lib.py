@@ -70,6 +70,11 @@ _SIGS = {
     "ss_validate_workspace_bytes": (u64, [u64]),
     "ss_count_distinct": (i32, [vp, u64, u32, vp, u64, C.POINTER(u64), vp]),
     "ss_count_distinct_workspace_bytes": (u64, [u64]),
+    "ss_csr_workspace_bytes": (u64, [u64, u64, C.POINTER(SSParams)]),
+    "ss_graph_transpose": (i32, [u64, u64, vp, vp, vp, vp, C.POINTER(SSParams), vp, u64,
+                                 C.POINTER(SSTelemetry), vp]),
+    "ss_csr_from_edges": (i32, [u64, u64, vp, vp, vp, vp, C.POINTER(SSParams), vp, u64,
+                                C.POINTER(SSTelemetry), vp]),
 }
 
 EXPORTS = tuple(_SIGS)

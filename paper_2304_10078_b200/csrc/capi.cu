@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "abi.cuh"
 #include "agg_engine.cuh"
 #include "engine.cuh"
 #include "sort_engine.cuh"
@@ -12,23 +13,6 @@
 namespace ss {
 
 thread_local std::string g_last_error;
-
-template <typename F>
-int guarded(F&& f) {
-  try {
-    f();
-    return SS_OK;
-  } catch (const Fail& e) {
-    g_last_error = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return SS_ERR_RESOURCE;
-  } catch (...) {
-    g_last_error = "unknown error";
-    return SS_ERR_RESOURCE;
-  }
-}
 
 // Calls f.template operator()<K, V>() for the runtime widths.
 template <typename F>
@@ -56,15 +40,6 @@ void dispatch_k(uint32_t kb, F&& f) {
   if (kb == 8) f.template operator()<uint64_t>();
   else if (kb == 4) f.template operator()<uint32_t>();
   else throw Fail(SS_ERR_CONTRACT, "key_bytes must be 4 or 8");
-}
-
-inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
-
-inline void reset_tel(ss_telemetry* t) {
-  if (!t) return;
-  int32_t timing = t->timing;
-  std::memset(t, 0, sizeof(*t));
-  t->timing = timing;
 }
 
 // ---------------------------------------------------------------------------
