@@ -244,6 +244,76 @@ def agg_main(args):
     print(json.dumps(line), flush=True)
 
 
+def graph_main(args):
+    """--workload graph: CSR transpose on a synthetic graph.
+
+    The paper's graphs (LJ/TW/CM/SD) are not in this container; a seeded
+    graph with Zipf(1.2) out-degrees and uniform targets over n/16 vertices
+    stands in (power-law sources, the social-graph shape).  Unit: Gedges/s
+    of transpose, input CSR resident, output allocated by the call.
+    """
+    import numpy as np
+    import torch
+
+    import paper_2304_10078_b200 as S
+    from paper_2304_10078_b200.datagen import generate_device
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    m = args.n
+    nv = max(1, m // 16)
+    src = generate_device("zipfian", 1.2, m, key_bits=32, seed=1, universe=nv, values="none", device=dev).keys
+    src = (src.to(torch.int64) - 1).to(torch.uint32)            # ranks 1..nv -> ids 0..nv-1
+    dst = generate_device("uniform", float(nv), m, key_bits=32, seed=2, values="none", device=dev).keys
+    g = S.from_edges(nv, src, dst)
+    del src, dst
+    params = S.TuningParams.for_input(m)
+
+    def one(tel=None):
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        t = S.transpose(g, params, telemetry=tel)
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), t
+
+    for _ in range(args.warmup):
+        one()
+    tel = S.Telemetry(timing=True)
+    times = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            dt, t = one(tel)
+            times.append(dt)
+            del t
+    ms = sum(times) / len(times)
+    cpu = None
+    if not args.no_cpu:   # the oracle transpose on a bounded sample (same shape, seed 1)
+        import oracle as O
+        ms_n = 1 << 20
+        rng = np.random.default_rng(1)
+        s_src = np.minimum(rng.zipf(1.2, ms_n) - 1, ms_n // 16 - 1).astype(np.uint32)
+        s_dst = rng.integers(0, ms_n // 16, ms_n).astype(np.uint32)
+        off, tg = O.csr_from_edges(ms_n // 16, s_src, s_dst)
+        t0 = time.perf_counter()
+        O.graph_transpose(ms_n // 16, off, tg)
+        tc = time.perf_counter() - t0
+        cpu = {"value": ms_n / tc / 1e9, "unit": "Gedges/s", "cores": 1, "kind": "port",
+               "sample": f"transpose of a {ms_n}-edge graph of the same shape; reference algorithm restated "
+                         f"in numpy (oracle/graphs_oracle.py), single thread, {tc:.2f} s"}
+    line = {"metric": "graph transpose Gedges/s (m=1e9 u32 edges, Zipf out-degrees)", "value": m / (ms / 1e3) / 1e9,
+            "unit": "Gedges/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (device-generated, seeded)",
+            "config": {"workload": f"graph: transpose, m={m} edges, n={nv} vertices, out-degree Zipf(1.2), "
+                                   "uniform targets", "params": "TuningParams.for_input(m)",
+                       "l2": "input (>= 4 GB) larger than the 126 MB L2"},
+            "phase_ms_per_step": {k: v / args.steps for k, v in tel.phase_ms.items()},
+            "gpu_launches": tel.kernel_launches, "clocks": clk.summary(), "e2e": None, "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+
+
 def reference_arm(args):
     """--impl reference: the CPU oracle port on a bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
@@ -292,8 +362,9 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=1 << 25)
     ap.add_argument("--ref-n", type=int, default=1 << 24)
     ap.add_argument("--validate", action="store_true", help="check the last output (O(n) device checks)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
-                    help="c2 (default, the headline semisort); c3 collect_reduce sum64; c4 histogram")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "graph"],
+                    help="c2 (default, the headline semisort); c3 collect_reduce sum64; c4 histogram; "
+                         "graph: CSR transpose")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -301,7 +372,7 @@ def main():
         return
     if args.workload != "c2":
         if int(os.environ.get("RANK", "0")) == 0:
-            agg_main(args)
+            graph_main(args) if args.workload == "graph" else agg_main(args)
         return
 
     import torch
