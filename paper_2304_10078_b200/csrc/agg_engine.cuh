@@ -177,7 +177,7 @@ k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, const
   V* rv = reinterpret_cast<V*>(rk + kLeafSmemMax);
   uint32_t* work = reinterpret_cast<uint32_t*>(SUM ? reinterpret_cast<unsigned char*>(rv + kLeafSmemMax)
                                                    : reinterpret_cast<unsigned char*>(rv));
-  // gsum (u64) leads the work arrays: keep it 8-byte aligned
+  // gsum (u64) follows the masks: keep the area 8-byte aligned
   work = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(work) + 15) & ~uintptr_t(15));
   for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
     const Leaf lf = leaves[l];

@@ -582,7 +582,7 @@ int ss_base_case(void* keys, void* values, uint64_t n, uint32_t key_bytes, uint3
                                                    1, scr, words);
       else
         k_leaf_eq_global<K, V><<<1, kLeafThreads, 0, st>>>(S_k, S_v, static_cast<K*>(keys), static_cast<V*>(values),
-                                                          d_leaf, 1, 1, identity, scr, words);
+                                                          d_leaf, 1, 1, identity, scr, words, hw_rank_ok() ? 1 : 0);
       check_launch();
       SS_CUDA(cudaStreamSynchronize(st));
     });

@@ -40,10 +40,14 @@ struct LeafArrays {
   unsigned long long* gsum;  // [m] (aggregation only) sum per first index
 };
 
-__host__ __device__ inline uint32_t leaf_cap(uint64_t m) {
+__host__ __device__ inline uint32_t leaf_cap(uint64_t m) {   // smallest pow2 >= 2m (>= 2)
+#ifdef __CUDA_ARCH__
+  return m <= 1 ? 2u : static_cast<uint32_t>(1ull << (64 - __clzll(2 * m - 1)));
+#else
   uint64_t c = 2;
   while (c < 2 * m) c <<= 1;
   return static_cast<uint32_t>(c);
+#endif
 }
 
 __host__ __device__ inline uint64_t leaf_words(uint64_t m, bool agg) {
@@ -54,14 +58,14 @@ __host__ __device__ inline uint64_t leaf_words(uint64_t m, bool agg) {
 __device__ __forceinline__ LeafArrays leaf_arrays(uint32_t* base, uint32_t cap, uint32_t m, bool agg) {
   LeafArrays a;
   uint32_t* p = base;
-  if (agg) {   // u64 first: keep it 8-byte aligned
+  a.mask = p; p += cap;   // cap is even: the u64 sums below stay 8-byte aligned
+  if (agg) {
     a.gsum = reinterpret_cast<unsigned long long*>(p);
     p += 2 * m + 2;
   } else {
     a.gsum = nullptr;
   }
   a.T = p; p += cap;
-  a.mask = p; p += cap;
   a.cnt = p; p += m;
   a.pos = p; p += m;
   a.arr = p;
@@ -77,7 +81,12 @@ __device__ __forceinline__ uint32_t leaf_probe(uint64_t h, uint32_t cap) {
 // Stable in-order ranks of one 32-wide item: `key` < mask capacity; `cur`
 // holds each key's cursor and advances by the item's count.
 __device__ __forceinline__ uint32_t warp_rank_item(bool valid, uint32_t key, uint32_t* mask, uint32_t* cur,
-                                                   uint32_t lane, uint32_t lt) {
+                                                   uint32_t lane, uint32_t lt, bool hw = false) {
+  if (hw) {   // lane-ordered atomicAdd returns (probe.cuh): the cursor is the rank
+    const uint32_t r = valid ? atomicAdd(&cur[key], 1u) : 0u;
+    __syncwarp();
+    return r;
+  }
   if (valid) atomicOr(&mask[key], 1u << lane);
   __syncwarp();
   const uint32_t peers = valid ? mask[key] : 0u;
@@ -108,7 +117,7 @@ __device__ __forceinline__ void warp_walk(const uint32_t* key_of, const uint32_t
 
 // Exclusive scan of a[0, L) in place (contiguous chunk per thread).
 __device__ inline void leaf_scan(uint32_t* a, uint32_t L, uint32_t* red) {
-  const uint32_t per = (L + blockDim.x - 1) / blockDim.x;
+  const uint32_t per = (L + blockDim.x - 1) >> (31 - __clz(blockDim.x));   // blockDim is a power of two
   const uint32_t c0 = min(L, threadIdx.x * per), c1 = min(L, c0 + per);
   uint32_t local = 0;
   for (uint32_t c = c0; c < c1; ++c) local += a[c];
@@ -126,7 +135,7 @@ __device__ inline void leaf_scan(uint32_t* a, uint32_t L, uint32_t* red) {
 // i's group, a.cnt[f] = size of the group whose first index is f (0 when f
 // is not a first index).  Returns whether every record shares one cell.
 template <typename K>
-__device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a) {
+__device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a, bool count = true) {
   __shared__ uint32_t s_cmin, s_cmax;
   const uint32_t cmask = cap - 1;
   for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
@@ -171,7 +180,7 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
     const uint32_t f = a.T[a.pos[i]];
     a.pos[i] = f;
-    atomicAdd(&a.cnt[f], 1u);
+    if (count) atomicAdd(&a.cnt[f], 1u);
   }
   __syncthreads();
   return s_cmin == s_cmax;
@@ -180,9 +189,10 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
 // Full semisort= leaf: records rk/rv (leaf-relative) -> ok/ov.
 template <typename K, typename V>
 __device__ void leaf_eq(const K* rk, const V* rv, K* ok, V* ov, uint32_t m, bool identity,
-                        LeafArrays a, uint32_t* red) {
+                        LeafArrays a, uint32_t* red, bool hw = false) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   const uint32_t cap = leaf_cap(m);
+  (void)hw;   // the CTA walk is one warp: its atomicOr ranks are not the bottleneck
   const bool one_cell = leaf_dedup(rk, m, cap, identity, a);
   leaf_scan(a.cnt, m, red);
   if (warp_id() == 0) warp_walk(a.pos, nullptr, m, a.mask, a.cnt, a.pos);   // pass 1
@@ -217,7 +227,7 @@ __host__ inline size_t leaf_smem_bytes(int key_bytes, int val_bytes) {
 template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
-               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity) {
+               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, int hw) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t red[33];
@@ -241,7 +251,7 @@ k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
     }
     __syncthreads();
     LeafArrays a = leaf_arrays(work, leaf_cap(m), m, false);
-    leaf_eq(rk, rv, dst_k + lf.lo, dst_v + lf.lo, m, identity != 0, a, red);
+    leaf_eq(rk, rv, dst_k + lf.lo, dst_v + lf.lo, m, identity != 0, a, red, hw != 0);
     __syncthreads();
   }
 }
@@ -275,7 +285,7 @@ template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_eq_global(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* __restrict__ A_v,
                  const Leaf* __restrict__ leaves, uint32_t n_leaves, int in_a, int identity,
-                 uint32_t* __restrict__ scratch, uint64_t words_per_cta) {
+                 uint32_t* __restrict__ scratch, uint64_t words_per_cta, int hw) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   __shared__ uint32_t red[33];
   uint32_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * words_per_cta;
@@ -299,7 +309,7 @@ k_leaf_eq_global(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, 
     }
     const uint32_t cap = leaf_cap(m);
     LeafArrays a = leaf_arrays(mine, cap, m, false);
-    leaf_eq(S_k + lf.lo, S_v + lf.lo, A_k + lf.lo, A_v + lf.lo, m, identity != 0, a, red);
+    leaf_eq(S_k + lf.lo, S_v + lf.lo, A_k + lf.lo, A_v + lf.lo, m, identity != 0, a, red, hw != 0);
     __syncthreads();
   }
 }

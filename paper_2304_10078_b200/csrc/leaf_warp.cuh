@@ -49,7 +49,7 @@ __device__ __forceinline__ void warp_excl_scan_vec(uint32_t* a, uint32_t L) {
 template <typename K, typename V, int ITEMS>
 __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                           K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t lo, uint32_t m,
-                                          bool identity, WarpLeafSmem<K>& ws) {
+                                          bool identity, WarpLeafSmem<K>& ws, bool hw) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   const uint32_t lane = lane_id(), lt = lanemask_lt();
   const uint32_t cap = leaf_cap_fast(m), cmask = cap - 1;
@@ -115,7 +115,7 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
   // pass 1: position in (first index, index) order
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
-    if (k < n_it) aux[k] = warp_rank_item(lane + 32 * k < m, aux[k], ws.mask, ws.cnt, lane, lt);
+    if (k < n_it) aux[k] = warp_rank_item(lane + 32 * k < m, aux[k], ws.mask, ws.cnt, lane, lt, hw);
   }
   if (!one_cell) {
     // pass 2: stable by cell over the pass-1 sequence
@@ -135,7 +135,7 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
       const uint32_t p = j * 32 + lane;
       const bool valid = p < m;
       const uint32_t c = valid ? ws.arr[p] : 0u;
-      const uint32_t d = warp_rank_item(valid, c, ws.mask, ws.T, lane, lt);
+      const uint32_t d = warp_rank_item(valid, c, ws.mask, ws.T, lane, lt, hw);
       if (valid) ws.dest[p] = static_cast<uint16_t>(d);
     }
     __syncwarp();
@@ -156,7 +156,7 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
 template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafWarpWarps * 32, 3)
 k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
-               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity) {
+               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, int hw) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   extern __shared__ __align__(16) unsigned char smem[];
   WarpLeafSmem<K>& ws = reinterpret_cast<WarpLeafSmem<K>*>(smem)[warp_id()];
@@ -175,7 +175,7 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       continue;
     }
     // one instantiation: several inlined variants cost registers (occupancy)
-    warp_leaf<K, V, kLeafWarpItems>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws);
+    warp_leaf<K, V, kLeafWarpItems>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws, hw != 0);
   }
 }
 

@@ -279,7 +279,8 @@ struct SortEngine {
     const size_t sm = sizeof(WarpLeafSmem<K>) * kLeafWarpWarps;
     SS_CUDA(cudaFuncSetAttribute(k_leaf_eq_warp<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     k_leaf_eq_warp<K, V><<<grid, kLeafWarpWarps * 32, sm, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v,
-                                                               d_list, static_cast<uint32_t>(count), identity);
+                                                               d_list, static_cast<uint32_t>(count), identity,
+                                                               hw_rank_ok() ? 1 : 0);
     check_launch();
     tr.launched();
     if (tel) tel->leaves_smem += count;
@@ -299,7 +300,7 @@ struct SortEngine {
     SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, smem));
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
     kern<<<grid, kLeafThreads, smem, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v, d_list,
-                                           static_cast<uint32_t>(count), identity);
+                                           static_cast<uint32_t>(count), identity, hw_rank_ok() ? 1 : 0);
     check_launch();
     tr.launched();
     if (tel) tel->leaves_smem += count;
@@ -318,7 +319,8 @@ struct SortEngine {
                                                     in_a, scr, words);
     } else {
       k_leaf_eq_global<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list,
-                                                            static_cast<uint32_t>(count), in_a, identity, scr, words);
+                                                            static_cast<uint32_t>(count), in_a, identity, scr, words,
+                                                            hw_rank_ok() ? 1 : 0);
     }
     check_launch();
     tr.launched();
