@@ -21,6 +21,13 @@
 
 namespace ss {
 
+// Fold leaves up to this size keep records and work arrays in shared memory:
+// 2048 when the staged record (key, + value for sums) is <= 8 bytes, 1024
+// above (two staging buffers per CTA must leave room for >= 2 CTAs per SM).
+__host__ __device__ constexpr uint32_t agg_smem_max(int staged_bytes) { return staged_bytes <= 8 ? 2048u : 1024u; }
+template <typename K, typename V, bool SUM>
+constexpr uint32_t kFoldMax = agg_smem_max(static_cast<int>(sizeof(K)) + (SUM ? ValTraits<V>::bytes : 0));
+
 template <typename V> __device__ __forceinline__ uint64_t val_u64(const V& v) { return static_cast<uint64_t>(v); }
 template <> __device__ __forceinline__ uint64_t val_u64<NoVal>(const NoVal&) { return 0; }
 template <> __device__ __forceinline__ uint64_t val_u64<V16>(const V16& v) { return v.lo; }
@@ -161,32 +168,64 @@ __device__ void leaf_fold(const K* rk, const V* rv, uint32_t m, bool identity, L
   if (threadIdx.x == 0) *g_out = tot;
 }
 
-__host__ inline size_t leaf_fold_smem_bytes(int key_bytes, int val_bytes) {
-  return static_cast<size_t>(kLeafSmemMax) * (key_bytes + val_bytes) +
-         leaf_words(kLeafSmemMax, true) * 4 + 64;
+// Staging buffer of one leaf: the 16-byte aligned superset of its keys
+// (values), as Bulk16 plans it.
+__host__ __device__ constexpr size_t fold_buf_bytes(uint32_t maxm, int elem_bytes) {
+  return elem_bytes ? ((static_cast<size_t>(maxm) + 2 * (16 / elem_bytes)) * elem_bytes + 15) & ~size_t(15) : 0;
 }
 
+__host__ inline size_t leaf_fold_smem_bytes(int key_bytes, int val_bytes) {
+  const uint32_t maxm = agg_smem_max(key_bytes + val_bytes);
+  return 2 * (fold_buf_bytes(maxm, key_bytes) + fold_buf_bytes(maxm, val_bytes)) + leaf_words(maxm, true) * 4 + 64;
+}
+
+// SMEM folds: the next leaf's keys (and values) stream in by TMA bulk copies
+// into the second buffer while this leaf folds (the plain per-leaf load
+// left the CTA waiting on memory at 2 CTAs per SM).
 template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kLeafThreads)
-k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, const Leaf* __restrict__ leaves,
-                 uint32_t n_leaves, int identity, K* __restrict__ st_k, uint64_t* __restrict__ st_a,
-                 uint32_t* __restrict__ G) {
+k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, uint64_t n_src,
+                 const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, K* __restrict__ st_k,
+                 uint64_t* __restrict__ st_a, uint32_t* __restrict__ G) {
+  constexpr uint32_t kMax = kFoldMax<K, V, SUM>;
+  constexpr size_t kBK = fold_buf_bytes(kMax, sizeof(K));
+  constexpr size_t kBV = SUM ? fold_buf_bytes(kMax, ValTraits<V>::bytes) : 0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t red[33];
-  K* rk = reinterpret_cast<K*>(smem);
-  V* rv = reinterpret_cast<V*>(rk + kLeafSmemMax);
-  uint32_t* work = reinterpret_cast<uint32_t*>(SUM ? reinterpret_cast<unsigned char*>(rv + kLeafSmemMax)
-                                                   : reinterpret_cast<unsigned char*>(rv));
-  // gsum (u64) follows the masks: keep the area 8-byte aligned
-  work = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(work) + 15) & ~uintptr_t(15));
-  for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
+  __shared__ __align__(8) uint64_t bar[2];
+  auto bufK = [&](int b) { return reinterpret_cast<K*>(smem + b * (kBK + kBV)); };
+  auto bufV = [&](int b) { return reinterpret_cast<V*>(smem + b * (kBK + kBV) + kBK); };
+  uint32_t* work = reinterpret_cast<uint32_t*>(smem + 2 * (kBK + kBV));   // 16-byte aligned
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t l, int b) {   // thread 0: stage leaf l into buffer b
     const Leaf lf = leaves[l];
     const uint32_t m = static_cast<uint32_t>(lf.size);
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      rk[i] = src_k[lf.lo + i];
-      if (SUM) rv[i] = src_v[lf.lo + i];
-    }
-    __syncthreads();
+    const Bulk16<K> bk(src_k, n_src, lf.lo, m);
+    Bulk16<V> bv(src_v, n_src, lf.lo, m);
+    uint32_t bytes = bk.ok ? bk.bytes : 0;
+    if (SUM && bv.ok) bytes += bv.bytes;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bar[b], bytes);
+    if (bk.ok) bulk_g2s(bufK(b), bk.src, bk.bytes, &bar[b]);
+    if (SUM && bv.ok) bulk_g2s(bufV(b), bv.src, bv.bytes, &bar[b]);
+  };
+  if (threadIdx.x == 0 && blockIdx.x < n_leaves) issue(blockIdx.x, 0);
+  uint32_t it = 0;
+  for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x, ++it) {
+    const int b = it & 1;
+    if (threadIdx.x == 0 && l + gridDim.x < n_leaves) issue(l + gridDim.x, b ^ 1);   // buffer b^1 is free
+    const Leaf lf = leaves[l];
+    const uint32_t m = static_cast<uint32_t>(lf.size);
+    const Bulk16<K> bk(src_k, n_src, lf.lo, m);
+    const Bulk16<V> bv(src_v, n_src, lf.lo, m);
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const K* rk = bk.ok ? bufK(b) + bk.sh : src_k + lf.lo;   // misfit supersets read global
+    const V* rv = (!SUM || bv.ok) ? bufV(b) + bv.sh : src_v + lf.lo;
     const uint32_t cap = leaf_cap(m);
     LeafArrays a = leaf_arrays(work, cap, m, true);
     leaf_fold<K, V, SUM>(rk, rv, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l);
@@ -306,7 +345,7 @@ struct AggEngine {
     sample_grid = static_cast<uint32_t>(std::min<uint64_t>(kSampleGridMax, max_nodes));
     const uint64_t mmax = std::max<uint64_t>(1, std::min<uint64_t>(n, alpha > 1 ? alpha - 1 : 1));
     leafg_words = leaf_words(mmax, true);
-    leafg_grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kLeafGlobalGridMax, cdiv(n, kLeafSmemMax + 1))));
+    leafg_grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kLeafGlobalGridMax, cdiv(n, agg_smem_max(16) + 1))));   // kind-independent (the workspace query has no kind)
     max_pairs = std::max<uint64_t>(n, 1);
     d_out_k = a.take<K>(max_pairs);
     d_out_a = a.take<uint64_t>(max_pairs);
@@ -345,6 +384,9 @@ struct AggEngine {
   }
 
   bool sum() const { return kind == SS_AGG_SUM64; }
+  uint32_t fold_max() const {   // the SMEM fold's leaf bound for this engine's staged record
+    return agg_smem_max(static_cast<int>(sizeof(K)) + (sum() ? ValTraits<V>::bytes : 0));
+  }
 
   // fold + emit one device leaf list living in `src`
   void fold_list(Tracker& tr, const K* sk, const V* sv, const Leaf* d_list, uint64_t count, bool smem_ok,
@@ -358,7 +400,7 @@ struct AggEngine {
         int per_sm = 0;
         SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, sm));
         const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
-        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G);
+        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, n, d_list, cnt, identity, st_k, st_a, d_G);
       };
       if (sum()) launch(k_leaf_fold_smem<K, V, true>);
       else launch(k_leaf_fold_smem<K, V, false>);
@@ -387,7 +429,7 @@ struct AggEngine {
     const uint64_t mmax = std::max<uint64_t>(1, std::min<uint64_t>(n, P.base_case_cutoff > 1 ? P.base_case_cutoff - 1 : 1));
     for (const Leaf& l : leaves) {
       SS_CUDA(cudaMemcpyAsync(d_leaf_g, &l, sizeof(Leaf), cudaMemcpyHostToDevice, st));
-      if (l.size <= kLeafSmemMax) {
+      if (l.size <= fold_max()) {
         fold_list(tr, sk, sv, d_leaf_g, 1, true, nullptr, 0, 1);
       } else if (l.size <= mmax) {
         fold_list(tr, sk, sv, d_leaf_g, 1, false, d_leafscr, leafg_words, 1);
@@ -486,7 +528,7 @@ struct AggEngine {
 
     tr.begin(kPhChildren);
     SS_CUDA(cudaMemsetAsync(d_misc, 0, 5 * sizeof(uint64_t), st));
-    const LeafClasses lcls{0, kLeafSmemMax, P.base_case_cutoff};
+    const LeafClasses lcls{0, fold_max(), P.base_case_cutoff};
     k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt);
     k_children_scan<<<1, 1024, 0, st>>>(d_ccnt, nn, d_misc);
     k_children_emit<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt, d_nbase,
