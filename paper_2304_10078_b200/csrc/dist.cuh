@@ -196,7 +196,16 @@ struct TileDesc {
 // to its data (the mbarrier phase that delivers the bytes also orders the
 // descriptor: arrive = release, try_wait = acquire), and ends with an exit
 // marker (cnt = 0).  A work item's tiles stay on one CTA, in order.
-template <typename K, typename V, typename Cfg>
+// A (key, value) record of the pair scratch layout (K == V): keys at even,
+// values at odd K-words (sort_engine.cuh, SortEngine::aos).
+template <typename K>
+struct alignas(2 * sizeof(K)) Pair2 {
+  K k, v;
+};
+
+// SA: the source is an array of Pair2<K> records (one bulk copy per tile
+// into the key + value areas of the stage) instead of two SoA columns.
+template <typename K, typename V, typename Cfg, bool SA = false>
 __device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __restrict__ sk, const V* __restrict__ sv,
                                               const uint16_t* __restrict__ ids, uint64_t n_src,
                                               const Work* __restrict__ work, uint32_t n_work, uint32_t* ctr,
@@ -242,23 +251,31 @@ __device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __re
     d.pad = 0;
     sdesc[b] = d;
     const Bulk16<uint16_t> bi(ids, n_src, begin, cnt);
-    const Bulk16<K> bk(sk, n_src, begin, cnt);
-    uint32_t bytes = bi.bytes + bk.bytes;
-    Bulk16<V> bv(sv, n_src, begin, cnt);
-    if constexpr (kHasV) bytes += bv.bytes;
-    fence_proxy_async();
-    mbar_arrive_expect_tx(&full[b], bytes);
-    if (l2_hint) {
+    if constexpr (SA) {   // pair records: one stream into the key + value areas
+      const Bulk16<Pair2<K>> bp(reinterpret_cast<const Pair2<K>*>(sk), n_src, begin, cnt);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full[b], bi.bytes + bp.bytes);
       if (bi.ok) bulk_g2s_hint(stI(b), bi.src, bi.bytes, &full[b], pol);
-      if (bk.ok) bulk_g2s_hint(stK(b), bk.src, bk.bytes, &full[b], pol);
-      if constexpr (kHasV) {
-        if (bv.ok) bulk_g2s_hint(stV(b), bv.src, bv.bytes, &full[b], pol);
-      }
+      if (bp.ok) bulk_g2s_hint(stK(b), bp.src, bp.bytes, &full[b], pol);
     } else {
-      if (bi.ok) bulk_g2s(stI(b), bi.src, bi.bytes, &full[b]);
-      if (bk.ok) bulk_g2s(stK(b), bk.src, bk.bytes, &full[b]);
-      if constexpr (kHasV) {
-        if (bv.ok) bulk_g2s(stV(b), bv.src, bv.bytes, &full[b]);
+      const Bulk16<K> bk(sk, n_src, begin, cnt);
+      const Bulk16<V> bv(sv, n_src, begin, cnt);
+      uint32_t bytes = bi.bytes + bk.bytes;
+      if constexpr (kHasV) bytes += bv.bytes;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full[b], bytes);
+      if (l2_hint) {
+        if (bi.ok) bulk_g2s_hint(stI(b), bi.src, bi.bytes, &full[b], pol);
+        if (bk.ok) bulk_g2s_hint(stK(b), bk.src, bk.bytes, &full[b], pol);
+        if constexpr (kHasV) {
+          if (bv.ok) bulk_g2s_hint(stV(b), bv.src, bv.bytes, &full[b], pol);
+        }
+      } else {
+        if (bi.ok) bulk_g2s(stI(b), bi.src, bi.bytes, &full[b]);
+        if (bk.ok) bulk_g2s(stK(b), bk.src, bk.bytes, &full[b]);
+        if constexpr (kHasV) {
+          if (bv.ok) bulk_g2s(stV(b), bv.src, bv.bytes, &full[b]);
+        }
       }
     }
     ptb += T;

@@ -40,7 +40,15 @@ struct Dist1Cfg : DistCfg<K, V, TILE, NT, STAGES> {
   }
 };
 
-template <typename K, typename V, int TILE, int NT, int STAGES>
+// SA: source in the pair scratch layout (keys at even, values at odd
+// K-words; sk points at the first key, sv is unused); DA: destination in
+// the pair layout -- a light record leaves as ONE 16-byte (8-byte for u32)
+// store instead of two partial-sector stores, a heavy record writes only
+// its value at K-word hbase + d of the pair array, hbase = start of the
+// node's heavy region, so a node's heavy values lie contiguous inside its
+// heavy region's own words [2 hbase, hbase + h1) (the copy-back streams them;
+// keys are filled there).  Both need V == K.
+template <typename K, typename V, int TILE, int NT, int STAGES, bool SA = false, bool DA = false>
 __global__ void __launch_bounds__(NT + 32, 1)   // 17 warps: one sub-partition holds 5 -> <= 96 registers
 
 k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
@@ -80,12 +88,13 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
   }
   __syncthreads();
   if (w == NW) {
-    if (lane == 0) dist_producer<K, V, Cfg>(smem, sk, sv, ids, n_src, work, n_work, ctr, full, empty, sdesc, dbg);
+    if (lane == 0) dist_producer<K, V, Cfg, SA>(smem, sk, sv, ids, n_src, work, n_work, ctr, full, empty, sdesc, dbg);
     return;
   }
 
   uint32_t nb = 0, npairs = 0;
   uint64_t rbase = 0;   // X[row][0]: positions below are relative to it
+  uint64_t hbase = 0;   // DA: start of the node's heavy region (X[node's first row][n_light])
   uint32_t* mine = cntw + w * pstride;
   const bool prof = (dbg & 4) && threadIdx.x == 0;
   unsigned long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tlast = prof ? clock64() : 0;
@@ -109,14 +118,26 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
       npairs = (nb + 1) >> 1;
       const uint64_t* xrow = X + td.row * stride;
       rbase = xrow[0];   // bucket-major layout: bucket 0's cursor is the row minimum
+      if constexpr (DA) hbase = n_light < nb ? X[static_cast<uint64_t>(nodes[td.node].row_base) * stride + n_light] : 0;
       for (uint32_t b = threadIdx.x; b < nb; b += NT) cursor[b] = static_cast<uint32_t>(xrow[b] - rbase);
     }
     const Bulk16<uint16_t> pi(ids, n_src, begin, cnt);
+    static_assert(!(SA || DA) || (sizeof(K) == sizeof(V) && ValTraits<V>::bytes == sizeof(K)), "pair layout needs V == K");
+    const Pair2<K>* gP = reinterpret_cast<const Pair2<K>*>(sk);
+    const Bulk16<Pair2<K>> pp(gP, n_src, begin, cnt);
     const Bulk16<K> pk(sk, n_src, begin, cnt);
     const Bulk16<V> pv(sv, n_src, begin, cnt);
+    const Pair2<K>* tP = reinterpret_cast<const Pair2<K>*>(stK(buf)) + pp.sh;
+    const bool staged = SA ? pp.ok : (pk.ok && (!kHasV || pv.ok));
+    auto rec_key = [&](uint32_t i) -> K {   // record i of the tile, staged or from global
+      if constexpr (SA) return staged ? tP[i].k : gP[begin + i].k;
+      else return pk.ok ? stK(buf)[pk.sh + i] : sk[begin + i];
+    };
+    auto rec_val = [&](uint32_t i) -> V {
+      if constexpr (SA) return static_cast<V>(staged ? tP[i].v : gP[begin + i].v);
+      else return pv.ok ? stV(buf)[pv.sh + i] : sv[begin + i];
+    };
     const uint16_t* tI = stI(buf) + pi.sh;
-    const K* tK = stK(buf) + pk.sh;
-    const V* tV = stV(buf) + pv.sh;
     mark(0);
 
     // A. in-warp ranks: old value of the warp's packed counter
@@ -253,7 +274,7 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
 #pragma unroll
         for (int v = 0; v < NW; ++v) cntw[v * pstride + j] = 0;
     }
-    if (pk.ok && (!kHasV || pv.ok) && !(dbg & 3)) {
+    if (staged && !(dbg & 3)) {
       constexpr int kB = ITEMS >= 4 ? 4 : ITEMS;
 #pragma unroll
       for (int k0 = 0; k0 < ITEMS; k0 += kB) {
@@ -269,14 +290,20 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
           const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
           wk[k] = ok[k] && b < key_below;
           dd[k] = rbase + static_cast<uint32_t>(wbase[b] + s);
-          kk[k] = tK[i];
-          if constexpr (kHasV) vv[k] = tV[i];
+          kk[k] = rec_key(i);
+          if constexpr (kHasV) vv[k] = rec_val(i);
         }
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
-          if (wk[k]) dk[dd[k]] = kk[k];
-          if constexpr (kHasV) {
-            if (ok[k]) dv[dd[k]] = vv[k];
+          if constexpr (DA) {
+            Pair2<K>* dP = reinterpret_cast<Pair2<K>*>(dk);
+            if (wk[k]) dP[dd[k]] = Pair2<K>{kk[k], static_cast<K>(vv[k])};
+            else if (ok[k]) reinterpret_cast<K*>(dk)[hbase + dd[k]] = static_cast<K>(vv[k]);
+          } else {
+            if (wk[k]) dk[dd[k]] = kk[k];
+            if constexpr (kHasV) {
+              if (ok[k]) dv[dd[k]] = vv[k];
+            }
           }
         }
       }
@@ -287,8 +314,13 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
         uint64_t d = rbase + static_cast<uint32_t>(wbase[b] + s);
         if (dbg & 2) d = begin + s;
         if (!(dbg & 1)) {
-          if (b < key_below) dk[d] = pk.ok ? tK[i] : sk[begin + i];
-          if constexpr (kHasV) dv[d] = pv.ok ? tV[i] : sv[begin + i];
+          if constexpr (DA) {
+            if (b < key_below) reinterpret_cast<Pair2<K>*>(dk)[d] = Pair2<K>{rec_key(i), static_cast<K>(rec_val(i))};
+            else reinterpret_cast<K*>(dk)[hbase + d] = static_cast<K>(rec_val(i));
+          } else {
+            if (b < key_below) dk[d] = rec_key(i);
+            if constexpr (kHasV) dv[d] = rec_val(i);
+          }
         }
       }
     }

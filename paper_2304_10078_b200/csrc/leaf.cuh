@@ -227,7 +227,8 @@ __host__ inline size_t leaf_smem_bytes(int key_bytes, int val_bytes) {
 template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
-               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, int hw) {
+               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, int hw,
+               uint32_t ss = 1) {   // ss 2: the leaves live in the pair scratch layout
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t red[33];
@@ -240,14 +241,14 @@ k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
     const uint32_t m = static_cast<uint32_t>(lf.size);
     if (m == 1) {
       if (threadIdx.x == 0 && src_k != dst_k) {
-        dst_k[lf.lo] = src_k[lf.lo];
-        if constexpr (kHasV) dst_v[lf.lo] = src_v[lf.lo];
+        dst_k[lf.lo] = src_k[lf.lo * ss];
+        if constexpr (kHasV) dst_v[lf.lo] = src_v[lf.lo * ss];
       }
       continue;
     }
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      rk[i] = src_k[lf.lo + i];
-      if constexpr (kHasV) rv[i] = src_v[lf.lo + i];
+      rk[i] = src_k[(lf.lo + i) * ss];
+      if constexpr (kHasV) rv[i] = src_v[(lf.lo + i) * ss];
     }
     __syncthreads();
     LeafArrays a = leaf_arrays(work, leaf_cap(m), m, false);
@@ -279,37 +280,69 @@ struct WarpLeafSmem {
   uint16_t dest[kLeafWarpMax];               // pass 2: final position of each pass-1 position
 };
 
+// SoA staging of one scratch-side leaf for the CTA kernels below: sk / sv
+// receive the leaf's records (leaf-relative).  Without the pair layout the
+// staging is S's own range; with it (s_pairs), the leaf's 2m K-words of
+// the pair array are viewed as m keys then m values -- a leaf living there
+// (!in_a) is first unpacked to its final range in A, which is free, and
+// restaged from A like an A-resident leaf.
+template <typename K, typename V>
+__device__ __forceinline__ void leaf_stage(K* S_k, V* S_v, K* A_k, V* A_v, const Leaf& lf, int in_a, int s_pairs,
+                                           K*& sk, V*& sv) {
+  constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  const uint32_t m = static_cast<uint32_t>(lf.size);
+  if (s_pairs) {
+    K* base = S_k + 2 * lf.lo;
+    sk = base;
+    sv = reinterpret_cast<V*>(base + m);
+    if (!in_a) {   // pairs -> A
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const K k = base[2 * i];
+        const K v = base[2 * i + 1];
+        A_k[lf.lo + i] = k;
+        if constexpr (kHasV) A_v[lf.lo + i] = static_cast<V>(v);
+      }
+      __syncthreads();
+    }
+  } else {
+    sk = S_k + lf.lo;
+    sv = S_v + lf.lo;
+    if (!in_a) return;
+  }
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {   // A -> staging
+    sk[i] = A_k[lf.lo + i];
+    if constexpr (kHasV) sv[i] = A_v[lf.lo + i];
+  }
+  __syncthreads();
+}
+
 // Leaves with work arrays in global scratch (any size).  If the leaf lives
 // in A (in_a), it is first copied to the free S range, then S -> A.
 template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_eq_global(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* __restrict__ A_v,
                  const Leaf* __restrict__ leaves, uint32_t n_leaves, int in_a, int identity,
-                 uint32_t* __restrict__ scratch, uint64_t words_per_cta, int hw) {
+                 uint32_t* __restrict__ scratch, uint64_t words_per_cta, int hw, int s_pairs = 0) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   __shared__ uint32_t red[33];
   uint32_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * words_per_cta;
   for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
     const Leaf lf = leaves[l];
     const uint32_t m = static_cast<uint32_t>(lf.size);
-    if (in_a) {
-      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        S_k[lf.lo + i] = A_k[lf.lo + i];
-        if constexpr (kHasV) S_v[lf.lo + i] = A_v[lf.lo + i];
-      }
-      __syncthreads();
-    }
+    K* sk;
+    V* sv;
+    leaf_stage(S_k, S_v, A_k, A_v, lf, in_a, s_pairs, sk, sv);
     if (m <= 1) {
       if (m == 1 && threadIdx.x == 0) {
-        A_k[lf.lo] = S_k[lf.lo];
-        if constexpr (kHasV) A_v[lf.lo] = S_v[lf.lo];
+        A_k[lf.lo] = sk[0];
+        if constexpr (kHasV) A_v[lf.lo] = sv[0];
       }
       __syncthreads();
       continue;
     }
     const uint32_t cap = leaf_cap(m);
     LeafArrays a = leaf_arrays(mine, cap, m, false);
-    leaf_eq(S_k + lf.lo, S_v + lf.lo, A_k + lf.lo, A_v + lf.lo, m, identity != 0, a, red, hw != 0);
+    leaf_eq(sk, sv, A_k + lf.lo, A_v + lf.lo, m, identity != 0, a, red, hw != 0);
     __syncthreads();
   }
 }
@@ -345,25 +378,21 @@ template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_lt(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* __restrict__ A_v,
           const Leaf* __restrict__ leaves, uint32_t n_leaves, int in_a,
-          uint32_t* __restrict__ scratch, uint64_t words_per_cta) {
+          uint32_t* __restrict__ scratch, uint64_t words_per_cta, int s_pairs = 0) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   uint32_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * words_per_cta;
   for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
     const Leaf lf = leaves[l];
     const uint32_t m = static_cast<uint32_t>(lf.size);
-    if (in_a) {
-      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        S_k[lf.lo + i] = A_k[lf.lo + i];
-        if constexpr (kHasV) S_v[lf.lo + i] = A_v[lf.lo + i];
-      }
-      __syncthreads();
-    }
+    K* sk;
+    V* sv;
+    leaf_stage(S_k, S_v, A_k, A_v, lf, in_a, s_pairs, sk, sv);
     uint32_t N = 1;
     while (N < m) N <<= 1;
     K* key = reinterpret_cast<K*>(mine);
     uint32_t* idx = reinterpret_cast<uint32_t*>(key + N);
     for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
-      key[i] = i < m ? S_k[lf.lo + i] : K(0);
+      key[i] = i < m ? sk[i] : K(0);
       idx[i] = i < m ? i : kEmpty32;
     }
     __syncthreads();
@@ -371,7 +400,7 @@ k_leaf_lt(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* __re
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       const uint32_t src = idx[i];
       A_k[lf.lo + i] = key[i];
-      if constexpr (kHasV) A_v[lf.lo + i] = S_v[lf.lo + src];
+      if constexpr (kHasV) A_v[lf.lo + i] = sv[src];
     }
     __syncthreads();
   }

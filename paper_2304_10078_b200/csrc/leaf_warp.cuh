@@ -49,7 +49,7 @@ __device__ __forceinline__ void warp_excl_scan_vec(uint32_t* a, uint32_t L) {
 template <typename K, typename V, int ITEMS>
 __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                           K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t lo, uint32_t m,
-                                          bool identity, WarpLeafSmem<K>& ws, bool hw) {
+                                          bool identity, WarpLeafSmem<K>& ws, bool hw, uint32_t ss) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   const uint32_t lane = lane_id(), lt = lanemask_lt();
   const uint32_t cap = leaf_cap_fast(m), cmask = cap - 1;
@@ -65,8 +65,8 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
     cell[k] = 0;
     aux[k] = 0;
     if (k < n_it && i < m) {
-      key[k] = src_k[lo + i];
-      if constexpr (kHasV) val[k] = src_v[lo + i];
+      key[k] = src_k[(lo + i) * ss];   // ss 2: the leaf lives in the pair scratch layout
+      if constexpr (kHasV) val[k] = src_v[(lo + i) * ss];
       ws.keys[i] = key[k];
       const uint64_t h = key_hash(key[k], identity);
       cell[k] = static_cast<uint32_t>(h) & cmask;
@@ -156,7 +156,8 @@ __device__ __forceinline__ void warp_leaf(const K* __restrict__ src_k, const V* 
 template <typename K, typename V>
 __global__ void __launch_bounds__(kLeafWarpWarps * 32, 3)
 k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __restrict__ dst_k,
-               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, int hw) {
+               V* __restrict__ dst_v, const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, int hw,
+               uint32_t ss = 1) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   extern __shared__ __align__(16) unsigned char smem[];
   WarpLeafSmem<K>& ws = reinterpret_cast<WarpLeafSmem<K>*>(smem)[warp_id()];
@@ -169,13 +170,13 @@ k_leaf_eq_warp(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
     const uint32_t m = static_cast<uint32_t>(lf.size);
     if (m <= 1) {
       if (m == 1 && lane_id() == 0 && src_k != dst_k) {
-        dst_k[lf.lo] = src_k[lf.lo];
-        if constexpr (kHasV) dst_v[lf.lo] = src_v[lf.lo];
+        dst_k[lf.lo] = src_k[lf.lo * ss];
+        if constexpr (kHasV) dst_v[lf.lo] = src_v[lf.lo * ss];
       }
       continue;
     }
     // one instantiation: several inlined variants cost registers (occupancy)
-    warp_leaf<K, V, kLeafWarpItems>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws, hw != 0);
+    warp_leaf<K, V, kLeafWarpItems>(src_k, src_v, dst_k, dst_v, lf.lo, m, ident, ws, hw != 0, ss);
   }
 }
 

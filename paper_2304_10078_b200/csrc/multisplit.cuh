@@ -84,7 +84,7 @@ template <typename K, typename BF>
 __global__ void __launch_bounds__(kCountThreads, 6)
 k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_work,
         const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, BF bf,
-        uint16_t* __restrict__ ids_out) {
+        uint16_t* __restrict__ ids_out, uint32_t kstride = 1) {   // kstride 2: pair scratch layout
   extern __shared__ __align__(16) uint32_t cnt[];
   __shared__ HeavySmem tab;
   for (uint32_t wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
@@ -98,14 +98,14 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
     __syncthreads();
     const uint64_t begin = wk.begin;
     const uint32_t len = wk.len;
-    const K* ws = src + begin;                                   // 32-bit offsets below
+    const K* ws = src + begin * kstride;                         // 32-bit offsets below
     uint16_t* wids = ids_out ? ids_out + begin : nullptr;
     constexpr uint32_t kBatch = kCountThreads * kCountItems;
     const uint32_t full = len - len % kBatch;
     for (uint32_t base = 0; base < full; base += kBatch) {      // no bounds checks
       K keys[kCountItems];
 #pragma unroll
-      for (int k = 0; k < kCountItems; ++k) keys[k] = __ldg(ws + base + k * kCountThreads + threadIdx.x);
+      for (int k = 0; k < kCountItems; ++k) keys[k] = __ldg(ws + (base + k * kCountThreads + threadIdx.x) * kstride);
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         const uint32_t i = base + k * kCountThreads + threadIdx.x;
@@ -119,7 +119,7 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
-        keys[k] = i < len ? __ldg(ws + i) : K(0);
+        keys[k] = i < len ? __ldg(ws + i * kstride) : K(0);
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
@@ -310,7 +310,8 @@ __device__ __forceinline__ void fill_span(K* __restrict__ dst, uint64_t lo, uint
 template <typename K, typename V>
 __global__ void k_copy_heavy_fill(K* __restrict__ dk, const V* __restrict__ sv, V* __restrict__ dv,
                                   const Node* __restrict__ nodes, uint32_t n_nodes, const uint64_t* __restrict__ off,
-                                  uint32_t stride, uint32_t n_light, const uint64_t* __restrict__ heavy, uint32_t mh) {
+                                  uint32_t stride, uint32_t n_light, const uint64_t* __restrict__ heavy, uint32_t mh,
+                                  int pairs = 0) {   // pairs: S is the pair layout (heavy values at words h0 + p)
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   __shared__ uint32_t s_t0;
   for (uint32_t j = blockIdx.y; j < n_nodes; j += gridDim.y) {
@@ -319,7 +320,10 @@ __global__ void k_copy_heavy_fill(K* __restrict__ dk, const V* __restrict__ sv, 
     const uint64_t h0 = o[0], h1 = nd.size;
     if (kHasV) {
       const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-      copy_span(dv, sv, nd.lo + h0, nd.lo + h1, tid, static_cast<uint64_t>(gridDim.x) * blockDim.x);
+      const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+      // pair layout: heavy value of position p at K-word h0abs + p (dist1.cuh)
+      const V* src = pairs ? reinterpret_cast<const V*>(reinterpret_cast<const K*>(sv) + nd.lo + h0) : sv;
+      copy_span(dv, src, nd.lo + h0, nd.lo + h1, tid, nth);
     }
     for (uint64_t c0 = h0 + blockIdx.x * kFillChunk; c0 < h1; c0 += gridDim.x * kFillChunk) {
       const uint64_t c1 = min(h1, c0 + kFillChunk);

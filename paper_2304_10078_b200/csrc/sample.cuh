@@ -105,7 +105,7 @@ template <typename K>
 __global__ void __launch_bounds__(kSampleThreads)
 k_sample(const K* __restrict__ src, Node* __restrict__ nodes, uint32_t n_nodes,
          uint64_t* __restrict__ heavy_out, uint64_t* __restrict__ scratch,
-         uint64_t s_cap, Params P, int use_fixed_key, uint64_t fixed_key) {
+         uint64_t s_cap, Params P, int use_fixed_key, uint64_t fixed_key, uint32_t kstride = 1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t red[33];
   __shared__ uint32_t n_cand;
@@ -162,7 +162,7 @@ k_sample(const K* __restrict__ src, Node* __restrict__ nodes, uint32_t n_nodes,
       uint64_t at = accepted + block_excl_scan<uint64_t>(mine_cnt, red, total);
       for (int w = 0; w < 8; ++w) {
         if (!(flags >> w & 1)) continue;
-        if (at < draws) samp[at] = static_cast<uint64_t>(src[lo + pos[w]]);
+        if (at < draws) samp[at] = static_cast<uint64_t>(src[(lo + pos[w]) * kstride]);   // 2: pair layout
         ++at;
       }
       accepted += total;

@@ -13,6 +13,7 @@
 #pragma once
 
 #include <cstdio>
+#include <type_traits>
 #include <vector>
 
 #include "engine.cuh"
@@ -30,9 +31,6 @@ constexpr uint64_t kMinChunk = 4096;
 constexpr uint32_t kSampleGridMax = 148;
 constexpr uint32_t kLeafGlobalGridMax = 296;
 constexpr size_t kSampleSmem = kSampleSmemCap * 4;
-constexpr int kDistShapeDefault = 0;
-constexpr uint64_t kCopySnapNodes = 4096;   // nodes whose heavy copy-back can run on the side stream
-constexpr uint32_t kCopySideCtas = 64;
 
 inline uint64_t lt_leaf_words(uint64_t m, int key_bytes) {
   return pow2_ge(std::max<uint64_t>(m, 1)) * (key_bytes + 4) / 4 + 16;
@@ -55,13 +53,13 @@ inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, u
   check_launch();
 }
 
-template <typename K, typename V, int TILE>
+template <typename K, typename V, int TILE, bool SA, bool DA>
 inline void launch_distribute1_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
                                  const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
                                  uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
                                  cudaStream_t st, uint32_t* ctr, uint32_t key_below) {
   const size_t dsm = Dist1Cfg<K, V, TILE, 512, 2>::smem_bytes(stride);
-  auto kern = k_distribute1<K, V, TILE, 512, 2>;
+  auto kern = k_distribute1<K, V, TILE, 512, 2, SA, DA>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
   const uint32_t grid = std::min<uint32_t>(nwork, 148u);
   SS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
@@ -76,27 +74,28 @@ inline bool dist_radix_forced() {
   return e && std::strcmp(e, "radix") == 0;
 }
 
-// Distribute launch shapes (SS_DIST_SHAPE, measurement knob):
-//   0: 512 threads, 1 CTA/SM, double-buffered tiles of 4096 (or smaller)
-//   1: 256 threads, 2 CTAs/SM, single-buffered 2048-record tiles
-//   2: 256 threads, 2 CTAs/SM, double-buffered 1024-record tiles
-// Shapes 1/2 apply while two CTAs fit shared memory, else shape 0.
-inline int dist_shape() {
-  static const int v = [] {
-    const char* e = std::getenv("SS_DIST_SHAPE");
-    return e ? std::atoi(e) : kDistShapeDefault;
-  }();
-  return v;
+// Tile of the single-pass kernel for this launch, 0 when the radix kernel
+// serves it (no hardware rank order, positions beyond u32, tables too big).
+template <typename K, typename V>
+inline int dist1_tile(uint32_t stride, uint64_t n_src) {
+  if (!hw_rank_ok() || dist_radix_forced() || n_src > 0xFFFFFFFFull) return 0;
+  if (Dist1Cfg<K, V, 4096, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) return 4096;
+  if (Dist1Cfg<K, V, 2048, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) return 2048;
+  return 0;
 }
 
 // Stable scatter of every work item through its X row, by the u16 bucket
 // ids `ids` the count pass stored; n_src = element count of the sources;
 // ctr = one workspace word (the dynamic work counter, zeroed here).
+// key_below: heavy buckets (>= key_below) do not write keys.  src_pairs /
+// dst_pairs: that side is the pair scratch layout (K == V, single-pass
+// kernel only; the caller checks dist1_tile).
 template <typename K, typename V>
 inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* dk, V* dv, const Work* d_work,
                               uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
                               uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st,
-                              uint64_t n_src, uint32_t* ctr, uint32_t key_below = 0xFFFFFFFFu) {
+                              uint64_t n_src, uint32_t* ctr, uint32_t key_below = 0xFFFFFFFFu,
+                              bool src_pairs = false, bool dst_pairs = false) {
   if (!nwork) return;
   static const int dbg = [] {
     const char* e = std::getenv("SS_DIST_DEBUG");
@@ -108,35 +107,32 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   if (stride >= kMaxDistBuckets) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
 #define SS_DIST_ARGS \
   sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light, fixed_nb, st, ctr
-  constexpr size_t kHalfSm = (228 * 1024) / 2 - 2048;   // two CTAs per SM
-  const int shape = dist_shape();
-  // single pass: hardware-ordered ranks, row-relative u32 positions, tables fit
-  bool done = false;
-  if (hw_rank_ok() && !dist_radix_forced() && n_src <= 0xFFFFFFFFull) {
-    if (Dist1Cfg<K, V, 4096, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) {
-      launch_distribute1_t<K, V, 4096>(SS_DIST_ARGS, key_below);
-      done = true;
-    } else if (Dist1Cfg<K, V, 2048, 512, 2>::smem_bytes(stride) <= kMaxDynSmem) {
-      launch_distribute1_t<K, V, 2048>(SS_DIST_ARGS, key_below);
-      done = true;
-    }
-  }
-  if (done) {
-  } else if (hw_rank_ok()) {
-    if (shape == 1 && DistCfg<K, V, 2048, 256, 1>::smem_bytes(stride) <= kHalfSm) {
-      launch_distribute_t<K, V, 2048, 256, 1, true>(SS_DIST_ARGS);
-    } else {
-      switch (dist_tile_for<K, V>(stride)) {
-        case 4096: launch_distribute_t<K, V, 4096, 512, 2, true>(SS_DIST_ARGS); break;
-        case 2048: launch_distribute_t<K, V, 2048, 512, 2, true>(SS_DIST_ARGS); break;
-        default: launch_distribute_t<K, V, 1024, 512, 2, true>(SS_DIST_ARGS);
+  const int t1 = dist1_tile<K, V>(stride, n_src);
+  if (t1) {
+    auto go = [&]<int TILE>() {
+      if constexpr (std::is_same_v<K, V>) {
+        if (src_pairs) return launch_distribute1_t<K, V, TILE, true, false>(SS_DIST_ARGS, key_below);
+        if (dst_pairs) return launch_distribute1_t<K, V, TILE, false, true>(SS_DIST_ARGS, key_below);
       }
-    }
+      launch_distribute1_t<K, V, TILE, false, false>(SS_DIST_ARGS, key_below);
+    };
+    if (t1 == 4096) go.template operator()<4096>();
+    else go.template operator()<2048>();
   } else {
+    if (src_pairs || dst_pairs) throw Fail(SS_ERR_RESOURCE, "pair scratch layout needs the single-pass distribute");
+    const bool hw = hw_rank_ok();
     switch (dist_tile_for<K, V>(stride)) {
-      case 4096: launch_distribute_t<K, V, 4096, 512, 2, false>(SS_DIST_ARGS); break;
-      case 2048: launch_distribute_t<K, V, 2048, 512, 2, false>(SS_DIST_ARGS); break;
-      default: launch_distribute_t<K, V, 1024, 512, 2, false>(SS_DIST_ARGS);
+      case 4096:
+        hw ? launch_distribute_t<K, V, 4096, 512, 2, true>(SS_DIST_ARGS)
+           : launch_distribute_t<K, V, 4096, 512, 2, false>(SS_DIST_ARGS);
+        break;
+      case 2048:
+        hw ? launch_distribute_t<K, V, 2048, 512, 2, true>(SS_DIST_ARGS)
+           : launch_distribute_t<K, V, 2048, 512, 2, false>(SS_DIST_ARGS);
+        break;
+      default:
+        hw ? launch_distribute_t<K, V, 1024, 512, 2, true>(SS_DIST_ARGS)
+           : launch_distribute_t<K, V, 1024, 512, 2, false>(SS_DIST_ARGS);
     }
   }
 #undef SS_DIST_ARGS
@@ -197,16 +193,16 @@ struct SortEngine {
   // workspace
   K* S_k = nullptr;
   V* S_v = nullptr;
+  // Pair scratch layout (K == V, chosen in run()): S holds (key, value)
+  // records, S_k = record base, S_v = S_k + 1, element stride 2.  Light
+  // records then leave the distribute as one 16-byte store instead of two
+  // partial-sector stores (the level-0 store path of c2 was bound by them).
+  bool aos = false;
+  uint32_t s_ss() const { return aos ? 2u : 1u; }
+  // where the copy-back reads heavy values: S_v, or the pair array's words
+  V* heavy_src() const { return aos ? reinterpret_cast<V*>(S_k) : S_v; }
   Node* d_nodes = nullptr;
   Node* d_next = nullptr;
-  Node* d_nodes_cp = nullptr;    // snapshot for the side-stream heavy copy
-  uint64_t* d_off_cp = nullptr;
-  uint64_t* d_heavy_cp = nullptr;
-  // side stream: heavy copy-back overlapped with the following levels
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  bool side_busy = false;
-  uint64_t snap_nodes = 0;
   uint64_t* d_heavy = nullptr;
   Work* d_work = nullptr;
   uint32_t* d_grp_node = nullptr;
@@ -238,8 +234,13 @@ struct SortEngine {
     leafg_words = std::max(leaf_words(mmax, false), lt_leaf_words(mmax, sizeof(K)));
     leafg_grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kLeafGlobalGridMax, cdiv(n, kLeafSmemMax + 1))));
     if (carve_scratch) {
-      S_k = a.take<K>(n);
-      if (kHasV) S_v = a.take<V>(n);
+      if constexpr (std::is_same_v<K, V>) {   // one 2n-word block: SoA halves or pair records
+        S_k = a.take<K>(2 * n);
+        S_v = reinterpret_cast<V*>(S_k + n);
+      } else {
+        S_k = a.take<K>(n);
+        if (kHasV) S_v = a.take<V>(n);
+      }
     }
     d_nodes = a.take<Node>(max_nodes);
     d_next = a.take<Node>(max_nodes);
@@ -250,10 +251,6 @@ struct SortEngine {
     d_X = a.take<uint64_t>(max_rows * stride);
     d_P = a.take<uint64_t>(max_grps * stride);
     d_off = a.take<uint64_t>(max_nodes * (stride + 1));
-    snap_nodes = std::min<uint64_t>(max_nodes, kCopySnapNodes);
-    d_nodes_cp = a.take<Node>(snap_nodes);
-    d_off_cp = a.take<uint64_t>(snap_nodes * (stride + 1));
-    d_heavy_cp = a.take<uint64_t>(snap_nodes * std::max<uint32_t>(P.max_heavy, 1));
     d_ccnt = a.take<uint32_t>(max_nodes * 4);
     d_misc = a.take<uint64_t>(8);
     d_ctr = a.take<uint32_t>(4);
@@ -280,7 +277,7 @@ struct SortEngine {
     SS_CUDA(cudaFuncSetAttribute(k_leaf_eq_warp<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     k_leaf_eq_warp<K, V><<<grid, kLeafWarpWarps * 32, sm, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v,
                                                                d_list, static_cast<uint32_t>(count), identity,
-                                                               hw_rank_ok() ? 1 : 0);
+                                                               hw_rank_ok() ? 1 : 0, in_a ? 1u : s_ss());
     check_launch();
     tr.launched();
     if (tel) tel->leaves_smem += count;
@@ -300,7 +297,8 @@ struct SortEngine {
     SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, smem));
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
     kern<<<grid, kLeafThreads, smem, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v, d_list,
-                                           static_cast<uint32_t>(count), identity, hw_rank_ok() ? 1 : 0);
+                                           static_cast<uint32_t>(count), identity, hw_rank_ok() ? 1 : 0,
+                                           in_a ? 1u : s_ss());
     check_launch();
     tr.launched();
     if (tel) tel->leaves_smem += count;
@@ -316,11 +314,11 @@ struct SortEngine {
     else grid = 1;
     if (mode == SS_MODE_LT) {
       k_leaf_lt<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count),
-                                                    in_a, scr, words);
+                                                    in_a, scr, words, aos ? 1 : 0);
     } else {
       k_leaf_eq_global<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list,
                                                             static_cast<uint32_t>(count), in_a, identity, scr, words,
-                                                            hw_rank_ok() ? 1 : 0);
+                                                            hw_rank_ok() ? 1 : 0, aos ? 1 : 0);
     }
     check_launch();
     tr.launched();
@@ -409,8 +407,9 @@ struct SortEngine {
     // sampling + heavy tables
     tr.begin(kPhSample);
     SS_CUDA(cudaFuncSetAttribute(k_sample<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSampleSmem)));
+    const uint32_t kss = from_a ? 1u : s_ss();   // key stride of the source side
     k_sample<K><<<std::min<uint32_t>(sample_grid, nn), kSampleThreads, kSampleSmem, st>>>(
-        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0);
+        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0, kss);
     check_launch();
     tr.launched();
 
@@ -424,7 +423,7 @@ struct SortEngine {
     // counting matrix
     tr.begin(kPhCount);
     k_count<K, KeyBuckets><<<nwork, kCountThreads, stride * 4, st>>>(sk, d_work, nwork, d_nodes, d_C, stride, bf,
-                                                                     d_ids);
+                                                                     d_ids, kss);
     check_launch();
     tr.launched();
 
@@ -443,43 +442,22 @@ struct SortEngine {
     tr.begin(kPhDistribute);
     // even levels (A -> S, copied back): heavy keys are filled by the copy
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu,
-                            P.light_buckets, 0, st, n, d_ctr, from_a ? P.light_buckets : 0xFFFFFFFFu);
+                            P.light_buckets, 0, st, n, d_ctr, from_a ? P.light_buckets : 0xFFFFFFFFu,
+                            aos && !from_a, aos && from_a);
     check_launch();
     tr.launched();
 
-    // heavy buckets are final: copy them back when they landed in S.  The
-    // copy touches only heavy ranges; every later step of the sort works on
-    // light ranges (disjoint), so it runs on a side stream, overlapped with
-    // the next level, from a snapshot of this level's nodes and offsets.
-    if (from_a && nn > snap_nodes) {   // wide level: copy in order on the main stream
+    // heavy buckets are final: copy them back when they landed in S (their
+    // keys were not scattered: one key per bucket, filled here).  In order on
+    // the caller's stream: overlapping it with the next level took SMs from
+    // the distribute (the two kernels cannot share an SM's registers).
+    if (from_a) {
       tr.begin(kPhCopy);
       const uint32_t gy = std::min<uint32_t>(nn, 65535);
       const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(1184, gy))));
-      k_copy_heavy_fill<K, V><<<dim3(gx, gy), 256, 0, st>>>(A_k, S_v, A_v, d_nodes, nn, d_off, stride,
-                                                           P.light_buckets, d_heavy, bf.max_heavy);
+      k_copy_heavy_fill<K, V><<<dim3(gx, gy), 256, 0, st>>>(A_k, heavy_src(), A_v, d_nodes, nn, d_off, stride,
+                                                           P.light_buckets, d_heavy, bf.max_heavy, aos ? 1 : 0);
       check_launch();
-      tr.launched();
-    } else if (from_a) {
-      tr.begin(kPhCopy);
-      if (side_busy) SS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));   // snapshot buffers free
-      SS_CUDA(cudaMemcpyAsync(d_nodes_cp, d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToDevice, st));
-      SS_CUDA(cudaMemcpyAsync(d_off_cp, d_off, nn * (stride + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-      SS_CUDA(cudaMemcpyAsync(d_heavy_cp, d_heavy, nn * bf.max_heavy * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-      SS_CUDA(cudaEventRecord(ev_fork, st));
-      SS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-      // few CTAs (bandwidth needs ~1/3 of the SMs): the next level's kernels
-      // keep the rest of the GPU
-      static const uint32_t side_ctas = [] {
-        const char* e = std::getenv("SS_COPY_CTAS");
-        return e ? static_cast<uint32_t>(std::atoi(e)) : kCopySideCtas;
-      }();
-      const uint32_t gy = std::min<uint32_t>(nn, side_ctas);
-      const uint32_t gx = static_cast<uint32_t>(std::max<uint64_t>(1, side_ctas / gy));
-      k_copy_heavy_fill<K, V><<<dim3(gx, gy), 512, 0, side>>>(A_k, S_v, A_v, d_nodes_cp, nn, d_off_cp, stride,
-                                                             P.light_buckets, d_heavy_cp, bf.max_heavy);
-      check_launch();
-      SS_CUDA(cudaEventRecord(ev_join, side));
-      side_busy = true;
       tr.launched();
     }
 
@@ -551,19 +529,12 @@ struct SortEngine {
   }
 
   void run(Tracker& tr) {
-    SS_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    SS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    SS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    struct Join {   // the caller's stream waits for the side stream on every exit
-      SortEngine* e;
-      ~Join() {
-        if (e->side_busy) cudaStreamWaitEvent(e->st, e->ev_join, 0);
-        cudaEventDestroy(e->ev_fork);
-        cudaEventDestroy(e->ev_join);
-        cudaStreamDestroy(e->side);   // released once its work completes
-        e->side_busy = false;
+    if constexpr (std::is_same_v<K, V>) {   // pair scratch layout when the single-pass kernel serves
+      if (!external_scratch && S_k && hw_rank_ok() && dist1_tile<K, V>(stride, n) != 0) {
+        aos = true;
+        S_v = reinterpret_cast<V*>(S_k + 1);
       }
-    } join{this};
+    }
     run_levels(tr);
   }
 
