@@ -53,33 +53,65 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and clock-event (throttle) reasons during the timed region.
 
+    Polls NVML every ~2 ms (a 5-step c2 run is ~130 ms; nvidia-smi at 0.2 s
+    saw one sample), falling back to nvidia-smi when NVML is unavailable.
+    """
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []   # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            bits = get_reasons(h)
+            self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx),
+                                 {name for name, bit in self.REASONS if bits & bit}))
+            self._stop.wait(0.002)
+
+    def _run_smi(self):
+        names = [name for name, _ in self.REASONS]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                    self.samples.append((float(f[0]), float(f[1]),
+                                         {n for n, v in zip(names, f[4:8]) if v.lower() == "active"}))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+        except Exception:
+            return self._run_smi()
+        try:
+            self._run_nvml(nv)
+        except Exception:
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.01)   # first sample before the timed region
         return self
 
     def __exit__(self, *exc):
@@ -88,17 +120,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for name, v in zip(names, s[4:8]):
-                if v.strip().lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [x[0] for x in self.samples]
+        reasons = set().union(*(x[2] for x in self.samples))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                "sm_min_mhz": min(sm), "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
 def cpu_baseline(n_sample: int, repeats: int = 1):
