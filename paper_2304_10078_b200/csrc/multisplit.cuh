@@ -15,6 +15,8 @@
 //               stores, and scatters each subarray stably through its X row.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "dist.cuh"
 #include "tma.cuh"
@@ -50,6 +52,11 @@ struct KeyBuckets {
   __device__ __forceinline__ uint32_t operator()(K key, uint64_t) const {
     return bucket_of(key, *tab, n_heavy, lc, identity != 0, n_light);
   }
+  // the kernel's own __shared__ table: no generic-to-shared conversions
+  template <typename K>
+  __device__ __forceinline__ uint32_t operator()(K key, uint64_t, const HeavySmem& t) const {
+    return bucket_of(key, t, n_heavy, lc, identity != 0, n_light);
+  }
 };
 
 // Precomputed ids (the reference's _counts_from_ids / _distribute_ids).
@@ -62,6 +69,10 @@ struct IdBuckets {
   template <typename K>
   __device__ __forceinline__ uint32_t operator()(K, uint64_t pos) const {
     return static_cast<uint32_t>(ids[pos]);
+  }
+  template <typename K>
+  __device__ __forceinline__ uint32_t operator()(K k, uint64_t pos, const HeavySmem&) const {
+    return (*this)(k, pos);
   }
 };
 
@@ -102,18 +113,22 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
     uint16_t* wids = ids_out ? ids_out + begin : nullptr;
     constexpr uint32_t kBatch = kCountThreads * kCountItems;
     const uint32_t full = len - len % kBatch;
-    for (uint32_t base = 0; base < full; base += kBatch) {      // no bounds checks
-      K keys[kCountItems];
+    auto full_batches = [&](auto write_ids) {   // no bounds checks; id store decided at compile time
+      for (uint32_t base = 0; base < full; base += kBatch) {
+        K keys[kCountItems];
 #pragma unroll
-      for (int k = 0; k < kCountItems; ++k) keys[k] = __ldg(ws + (base + k * kCountThreads + threadIdx.x) * kstride);
+        for (int k = 0; k < kCountItems; ++k) keys[k] = __ldg(ws + (base + k * kCountThreads + threadIdx.x) * kstride);
 #pragma unroll
-      for (int k = 0; k < kCountItems; ++k) {
-        const uint32_t i = base + k * kCountThreads + threadIdx.x;
-        const uint32_t b = bf(keys[k], begin + i);
-        atomicAdd(&cnt[b], 1u);
-        if (wids) wids[i] = static_cast<uint16_t>(b);           // consumed by k_distribute
+        for (int k = 0; k < kCountItems; ++k) {
+          const uint32_t i = base + k * kCountThreads + threadIdx.x;
+          const uint32_t b = bf(keys[k], begin + i, tab);
+          atomicAdd(&cnt[b], 1u);
+          if constexpr (decltype(write_ids)::value) wids[i] = static_cast<uint16_t>(b);   // consumed by k_distribute
+        }
       }
-    }
+    };
+    if (wids) full_batches(std::true_type{});
+    else full_batches(std::false_type{});
     for (uint32_t base = full; base < len; base += kBatch) {    // tail
       K keys[kCountItems];
 #pragma unroll

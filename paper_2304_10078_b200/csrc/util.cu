@@ -195,6 +195,10 @@ struct PartBuckets {
   __device__ __forceinline__ uint32_t operator()(K key, uint64_t) const {
     return shift >= 64 ? 0u : static_cast<uint32_t>(mix64(static_cast<uint64_t>(key)) >> shift);
   }
+  template <typename K>
+  __device__ __forceinline__ uint32_t operator()(K key, uint64_t pos, const HeavySmem&) const {
+    return (*this)(key, pos);
+  }
 };
 
 struct PartPlan {
