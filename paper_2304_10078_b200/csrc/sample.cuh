@@ -76,7 +76,11 @@ __device__ void sample_table_insert(E* tab, uint32_t cap, const uint64_t* samp, 
     uint32_t peers = __match_any_sync(act, key);
     if (lane_id() != __ffs(peers) - 1) continue;
     uint32_t c = __popc(peers);
-    uint32_t slot = static_cast<uint32_t>(mix64(key)) & mask;
+    // probe start from the top bits of a multiplicative hash of the folded
+    // mix: a node's keys share the low hash bits its ancestors bucketed on,
+    // so `mix64(key) & mask` would start every probe in a few slots
+    const uint64_t h = mix64(key);
+    uint32_t slot = (static_cast<uint32_t>(h ^ (h >> 32)) * 0x9E3779B1u) >> (32 - (31 - __clz(cap)));
     while (true) {
       E old = tab[slot];
       if (old == X::kEmpty) {
