@@ -12,6 +12,8 @@
 // by level, heavy pairs by node then leaves by (node, bucket).
 #pragma once
 
+#include <type_traits>
+
 #include "engine.cuh"
 #include "leaf.cuh"
 #include "multisplit.cuh"
@@ -37,7 +39,8 @@ template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kCountThreads)
 k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restrict__ work, uint32_t n_work,
             const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, KeyBuckets bf,
-            unsigned long long* __restrict__ HS, uint32_t hs_stride, uint16_t* __restrict__ ids_out) {
+            unsigned long long* __restrict__ HS, uint32_t hs_stride, uint16_t* __restrict__ ids_out,
+            uint32_t ss = 1) {   // ss 2: (key, value) pair records
   extern __shared__ __align__(16) uint32_t cnt[];
   __shared__ HeavySmem tab;
   // heavy partial sums as native 32-bit atomics: low half, carries out of
@@ -61,8 +64,8 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restric
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
-        keys[k] = i < len ? ldg_key(src, begin + i) : K(0);
-        if constexpr (SUM) vals[k] = i < len ? val_u64(sv[begin + i]) : 0ull;
+        keys[k] = i < len ? ldg_key(src, (begin + i) * ss) : K(0);
+        if constexpr (SUM) vals[k] = i < len ? val_u64(sv[(begin + i) * ss]) : 0ull;
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
@@ -125,16 +128,17 @@ __global__ void k_heavy_fold(const Node* __restrict__ nodes, uint32_t n_nodes, c
 
 // Base fold of one leaf: groups in chained-hash order, (cell, first index)
 // (aggregate.py:239-264), with count or sum; leaf.cuh's dedup and passes.
+// ss: element stride of rk / rv (2 for (key, value) pair records).
 template <typename K, typename V, bool SUM>
 __device__ void leaf_fold(const K* rk, const V* rv, uint32_t m, bool identity, LeafArrays a, uint32_t* red,
-                          K* out_k, uint64_t* out_a, uint32_t* g_out) {
+                          K* out_k, uint64_t* out_a, uint32_t* g_out, uint32_t ss = 1) {
   const uint32_t cap = leaf_cap(m);
   if (SUM)
     for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) a.gsum[f] = 0;
-  const bool one_cell = leaf_dedup(rk, m, cap, identity, a);
+  const bool one_cell = leaf_dedup(rk, m, cap, identity, a, true, ss);
   if (SUM)
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
-      atomicAdd(&a.gsum[a.pos[i]], static_cast<unsigned long long>(val_u64(rv[i])));
+      atomicAdd(&a.gsum[a.pos[i]], static_cast<unsigned long long>(val_u64(rv[i * ss])));
   // rank of each group (first index f) in (cell, f) order -> a.arr[f]
   if (one_cell) {
     for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) a.arr[f] = a.cnt[f] ? 1u : 0u;
@@ -145,7 +149,7 @@ __device__ void leaf_fold(const K* rk, const V* rv, uint32_t m, bool identity, L
     __syncthreads();
     for (uint32_t f = threadIdx.x; f < m; f += blockDim.x) {
       if (!a.cnt[f]) continue;
-      const uint32_t c = static_cast<uint32_t>(key_hash(rk[f], identity)) & (cap - 1);
+      const uint32_t c = static_cast<uint32_t>(key_hash(rk[f * ss], identity)) & (cap - 1);
       atomicAdd(&a.T[c], 1u);
       a.arr[f] = c;
     }
@@ -159,7 +163,7 @@ __device__ void leaf_fold(const K* rk, const V* rv, uint32_t m, bool identity, L
     const uint32_t c = a.cnt[f];
     if (!c) continue;
     const uint32_t g = a.arr[f];
-    out_k[g] = rk[f];
+    out_k[g] = rk[f * ss];
     out_a[g] = SUM ? static_cast<uint64_t>(a.gsum[f]) : c;
     ++groups;
   }
@@ -186,7 +190,10 @@ template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, uint64_t n_src,
                  const Leaf* __restrict__ leaves, uint32_t n_leaves, int identity, K* __restrict__ st_k,
-                 uint64_t* __restrict__ st_a, uint32_t* __restrict__ G) {
+                 uint64_t* __restrict__ st_a, uint32_t* __restrict__ G, uint32_t ss = 1) {
+  // ss 2: src_k is an array of (key, value) pair records (K == V, sums)
+  constexpr bool kPairsOk = SUM && std::is_same_v<K, V>;
+  const bool pairs = kPairsOk && ss == 2;
   constexpr uint32_t kMax = kFoldMax<K, V, SUM>;
   constexpr size_t kBK = fold_buf_bytes(kMax, sizeof(K));
   constexpr size_t kBV = SUM ? fold_buf_bytes(kMax, ValTraits<V>::bytes) : 0;
@@ -205,6 +212,15 @@ k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, uint6
   auto issue = [&](uint32_t l, int b) {   // thread 0: stage leaf l into buffer b
     const Leaf lf = leaves[l];
     const uint32_t m = static_cast<uint32_t>(lf.size);
+    if constexpr (kPairsOk) {
+      if (pairs) {   // one stream of pairs into the key + value areas
+        const Bulk16<Pair2<K>> bp(reinterpret_cast<const Pair2<K>*>(src_k), n_src, lf.lo, m);
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[b], bp.ok ? bp.bytes : 0u);
+        if (bp.ok) bulk_g2s(bufK(b), bp.src, bp.bytes, &bar[b]);
+        return;
+      }
+    }
     const Bulk16<K> bk(src_k, n_src, lf.lo, m);
     Bulk16<V> bv(src_v, n_src, lf.lo, m);
     uint32_t bytes = bk.ok ? bk.bytes : 0;
@@ -226,9 +242,16 @@ k_leaf_fold_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, uint6
     mbar_wait(&bar[b], (it >> 1) & 1);
     const K* rk = bk.ok ? bufK(b) + bk.sh : src_k + lf.lo;   // misfit supersets read global
     const V* rv = (!SUM || bv.ok) ? bufV(b) + bv.sh : src_v + lf.lo;
+    if constexpr (kPairsOk) {
+      if (pairs) {
+        const Bulk16<Pair2<K>> bp(reinterpret_cast<const Pair2<K>*>(src_k), n_src, lf.lo, m);
+        rk = bp.ok ? bufK(b) + 2 * bp.sh : src_k + 2 * lf.lo;
+        rv = reinterpret_cast<const V*>(rk + 1);
+      }
+    }
     const uint32_t cap = leaf_cap(m);
     LeafArrays a = leaf_arrays(work, cap, m, true);
-    leaf_fold<K, V, SUM>(rk, rv, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l);
+    leaf_fold<K, V, SUM>(rk, rv, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l, pairs ? 2u : 1u);
     __syncthreads();
   }
 }
@@ -237,14 +260,17 @@ template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_fold_global(const K* __restrict__ src_k, const V* __restrict__ src_v, const Leaf* __restrict__ leaves,
                    uint32_t n_leaves, int identity, K* __restrict__ st_k, uint64_t* __restrict__ st_a,
-                   uint32_t* __restrict__ G, uint32_t* __restrict__ scratch, uint64_t words_per_cta) {
+                   uint32_t* __restrict__ G, uint32_t* __restrict__ scratch, uint64_t words_per_cta,
+                   uint32_t ss = 1) {   // ss 2: (key, value) pair records at src_k
   __shared__ uint32_t red[33];
   uint32_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * words_per_cta;
   for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
     const Leaf lf = leaves[l];
     const uint32_t m = static_cast<uint32_t>(lf.size);
     LeafArrays a = leaf_arrays(mine, leaf_cap(m), m, true);
-    leaf_fold<K, V, SUM>(src_k + lf.lo, src_v + lf.lo, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l);
+    const K* rk = src_k + lf.lo * ss;
+    const V* rv = ss == 2 ? reinterpret_cast<const V*>(rk + 1) : src_v + lf.lo;
+    leaf_fold<K, V, SUM>(rk, rv, m, identity != 0, a, red, st_k + lf.lo, st_a + lf.lo, G + l, ss);
     __syncthreads();
   }
 }
@@ -351,8 +377,13 @@ struct AggEngine {
     d_out_a = a.take<uint64_t>(max_pairs);
     d_cursor = a.take<uint64_t>(1);
     for (int i = 0; i < 2; ++i) {
-      B_k[i] = a.take<K>(n);
-      if (kHasV) B_v[i] = a.take<V>(n);
+      if constexpr (std::is_same_v<K, V>) {   // one 2n-word block: SoA halves or pair records (run())
+        B_k[i] = a.take<K>(2 * n);
+        B_v[i] = reinterpret_cast<V*>(B_k[i] + n);
+      } else {
+        B_k[i] = a.take<K>(n);
+        if (kHasV) B_v[i] = a.take<V>(n);
+      }
     }
     st_k = a.take<K>(n);
     st_a = a.take<uint64_t>(n);
@@ -384,13 +415,18 @@ struct AggEngine {
   }
 
   bool sum() const { return kind == SS_AGG_SUM64; }
+  // Pair buffers (K == V, sum64, chosen in run()): B holds (key, value)
+  // records, element stride 2 -- the light scatter then writes one 16-byte
+  // record instead of two partial-sector stores (c3's level 0 is all light).
+  bool pairs = false;
+  uint32_t bss() const { return pairs ? 2u : 1u; }
   uint32_t fold_max() const {   // the SMEM fold's leaf bound for this engine's staged record
     return agg_smem_max(static_cast<int>(sizeof(K)) + (sum() ? ValTraits<V>::bytes : 0));
   }
 
   // fold + emit one device leaf list living in `src`
   void fold_list(Tracker& tr, const K* sk, const V* sv, const Leaf* d_list, uint64_t count, bool smem_ok,
-                 uint32_t* scr, uint64_t words, uint32_t grid_cap) {
+                 uint32_t* scr, uint64_t words, uint32_t grid_cap, uint32_t ss = 1) {
     if (!count) return;
     const uint32_t cnt = static_cast<uint32_t>(count);
     if (smem_ok) {
@@ -400,7 +436,7 @@ struct AggEngine {
         int per_sm = 0;
         SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, sm));
         const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
-        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, n, d_list, cnt, identity, st_k, st_a, d_G);
+        kern<<<grid, kLeafThreads, sm, st>>>(sk, sv, n, d_list, cnt, identity, st_k, st_a, d_G, ss);
       };
       if (sum()) launch(k_leaf_fold_smem<K, V, true>);
       else launch(k_leaf_fold_smem<K, V, false>);
@@ -409,10 +445,10 @@ struct AggEngine {
       const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, grid_cap));
       if (sum())
         k_leaf_fold_global<K, V, true><<<grid, kLeafThreads, 0, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G,
-                                                                     scr, words);
+                                                                     scr, words, ss);
       else
         k_leaf_fold_global<K, V, false><<<grid, kLeafThreads, 0, st>>>(sk, sv, d_list, cnt, identity, st_k, st_a, d_G,
-                                                                      scr, words);
+                                                                      scr, words, ss);
       if (tel) tel->leaves_global += count;
     }
     check_launch();
@@ -425,19 +461,19 @@ struct AggEngine {
   }
 
   // host-built leaves of any size (root leaf, forced leaves)
-  void fold_host(Tracker& tr, const K* sk, const V* sv, const std::vector<Leaf>& leaves) {
+  void fold_host(Tracker& tr, const K* sk, const V* sv, const std::vector<Leaf>& leaves, uint32_t ss = 1) {
     const uint64_t mmax = std::max<uint64_t>(1, std::min<uint64_t>(n, P.base_case_cutoff > 1 ? P.base_case_cutoff - 1 : 1));
     for (const Leaf& l : leaves) {
       SS_CUDA(cudaMemcpyAsync(d_leaf_g, &l, sizeof(Leaf), cudaMemcpyHostToDevice, st));
       if (l.size <= fold_max()) {
-        fold_list(tr, sk, sv, d_leaf_g, 1, true, nullptr, 0, 1);
+        fold_list(tr, sk, sv, d_leaf_g, 1, true, nullptr, 0, 1, ss);
       } else if (l.size <= mmax) {
-        fold_list(tr, sk, sv, d_leaf_g, 1, false, d_leafscr, leafg_words, 1);
+        fold_list(tr, sk, sv, d_leaf_g, 1, false, d_leafscr, leafg_words, 1, ss);
       } else {
         const uint64_t words = leaf_words(l.size, true);
         uint32_t* scr = nullptr;
         SS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scr), words * 4, st));
-        fold_list(tr, sk, sv, d_leaf_g, 1, false, scr, words, 1);
+        fold_list(tr, sk, sv, d_leaf_g, 1, false, scr, words, 1, ss);
         SS_CUDA(cudaFreeAsync(scr, st));
       }
       SS_CUDA(cudaStreamSynchronize(st));   // &l must outlive the copy
@@ -481,8 +517,9 @@ struct AggEngine {
 
     tr.begin(kPhSample);
     SS_CUDA(cudaFuncSetAttribute(k_sample<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSampleSmem)));
+    const uint32_t sss = lvl == 1 ? 1u : bss();   // element stride of the source side
     k_sample<K><<<std::min<uint32_t>(sample_grid, nn), kSampleThreads, kSampleSmem, st>>>(
-        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0);
+        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0, sss);
     check_launch();
     tr.launched();
 
@@ -496,10 +533,10 @@ struct AggEngine {
     tr.begin(kPhCount);
     if (sum())
       k_count_agg<K, V, true><<<nwork, kCountThreads, stride * 4, st>>>(sk, sv, d_work, nwork, d_nodes, d_C, stride, bf,
-                                                                        d_HS, mh, d_ids);
+                                                                        d_HS, mh, d_ids, sss);
     else
       k_count_agg<K, V, false><<<nwork, kCountThreads, stride * 4, st>>>(sk, sv, d_work, nwork, d_nodes, d_C, stride,
-                                                                         bf, d_HS, mh, d_ids);
+                                                                         bf, d_HS, mh, d_ids, sss);
     check_launch();
     tr.launched();
 
@@ -514,7 +551,8 @@ struct AggEngine {
 
     tr.begin(kPhDistribute);
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, P.light_buckets,
-                            P.light_buckets, 0, st, n, reinterpret_cast<uint32_t*>(d_misc + 7));
+                            P.light_buckets, 0, st, n, reinterpret_cast<uint32_t*>(d_misc + 7), 0xFFFFFFFFu,
+                            pairs && lvl > 1, pairs);
     tr.launched();
 
     tr.begin(kPhCopy);
@@ -579,21 +617,27 @@ struct AggEngine {
       check_launch();
       tr.launched(2);
     }
-    fold_list(tr, dk, dv, d_leaf_s, n_s, true, nullptr, 0, 1);
-    fold_list(tr, dk, dv, d_leaf_g, n_g, false, d_leafscr, leafg_words, leafg_grid);
+    fold_list(tr, dk, dv, d_leaf_s, n_s, true, nullptr, 0, 1, bss());
+    fold_list(tr, dk, dv, d_leaf_g, n_g, false, d_leafscr, leafg_words, leafg_grid, bss());
     std::vector<Node> keep;
     std::vector<Leaf> forced;
     for (const Node& c : next) {
       if (c.stalled >= 2 || lvl + 1 >= kDepthLimit) forced.push_back(Leaf{c.lo, c.size});
       else keep.push_back(c);
     }
-    fold_host(tr, dk, dv, forced);
+    fold_host(tr, dk, dv, forced, bss());
     SS_CUDA(cudaStreamSynchronize(st));   // hoff must outlive its copy
     tr.end();
     return keep;
   }
 
   uint64_t run(Tracker& tr) {
+    if constexpr (std::is_same_v<K, V>) {   // pair buffers when summing through the single-pass kernel
+      if (sum() && hw_rank_ok() && dist1_tile<K, V>(stride, n) != 0) {
+        pairs = true;
+        for (int i = 0; i < 2; ++i) B_v[i] = reinterpret_cast<V*>(B_k[i] + 1);
+      }
+    }
     SS_CUDA(cudaMemsetAsync(d_cursor, 0, sizeof(uint64_t), st));
     if (tel) {
       tel->nodes += 1;

@@ -134,8 +134,10 @@ __device__ inline void leaf_scan(uint32_t* a, uint32_t L, uint32_t* red) {
 // Step 1 + record counts per first index: a.pos[i] = first index of record
 // i's group, a.cnt[f] = size of the group whose first index is f (0 when f
 // is not a first index).  Returns whether every record shares one cell.
+// ks: element stride of rk (2 when the records are (key, value) pairs).
 template <typename K>
-__device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a, bool count = true) {
+__device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a, bool count = true,
+                           uint32_t ks = 1) {
   __shared__ uint32_t s_cmin, s_cmax;
   const uint32_t cmask = cap - 1;
   for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
@@ -150,7 +152,7 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
   __syncthreads();
   uint32_t cmin = 0xFFFFFFFFu, cmax = 0;
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const K k = rk[i];
+    const K k = rk[i * ks];
     const uint64_t h = key_hash(k, identity);
     const uint32_t c = static_cast<uint32_t>(h) & cmask;
     cmin = min(cmin, c);
@@ -162,7 +164,7 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
         t = atomicCAS(&a.T[s], kEmpty32, i);
         if (t == kEmpty32) break;
       }
-      if (rk[t] == k) {
+      if (rk[t * ks] == k) {
         if (i < t) atomicMin(&a.T[s], i);   // T[s] only decreases: skip when already smaller
         break;
       }

@@ -111,6 +111,7 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   if (t1) {
     auto go = [&]<int TILE>() {
       if constexpr (std::is_same_v<K, V>) {
+        if (src_pairs && dst_pairs) return launch_distribute1_t<K, V, TILE, true, true>(SS_DIST_ARGS, key_below);
         if (src_pairs) return launch_distribute1_t<K, V, TILE, true, false>(SS_DIST_ARGS, key_below);
         if (dst_pairs) return launch_distribute1_t<K, V, TILE, false, true>(SS_DIST_ARGS, key_below);
       }
