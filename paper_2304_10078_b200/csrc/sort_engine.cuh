@@ -18,6 +18,7 @@
 
 #include "engine.cuh"
 #include "leaf.cuh"
+#include "leaf_lt.cuh"
 #include "leaf_warp.cuh"
 #include "dist1.cuh"
 #include "multisplit.cuh"
@@ -268,8 +269,20 @@ struct SortEngine {
   // ---- leaves ---------------------------------------------------------------
   void run_leaves_warp(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a) {
     if (!count) return;
-    if (mode == SS_MODE_LT) {
-      run_leaves_global(tr, d_list, count, in_a, nullptr, 0);
+    if (mode == SS_MODE_LT) {   // semisort<: (key, index) bitonic per warp
+      const size_t sm = sizeof(LtWarpSmem<K, V>) * kLeafWarpWarps;
+      SS_CUDA(cudaFuncSetAttribute(k_leaf_lt_warp<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)));
+      int per_sm = 0;
+      SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leaf_lt_warp<K, V>, kLeafWarpWarps * 32, sm));
+      const uint32_t grid = static_cast<uint32_t>(
+          std::min<uint64_t>(cdiv(count, kLeafWarpWarps), 148u * std::max(per_sm, 1)));
+      k_leaf_lt_warp<K, V><<<grid, kLeafWarpWarps * 32, sm, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v,
+                                                                 d_list, static_cast<uint32_t>(count),
+                                                                 in_a ? 1u : s_ss());
+      check_launch();
+      tr.launched();
+      if (tel) tel->leaves_smem += count;
       return;
     }
     leaf_stats("warp", d_list, count, st);
@@ -286,8 +299,18 @@ struct SortEngine {
 
   void run_leaves_smem(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a) {
     if (!count) return;
-    if (mode == SS_MODE_LT) {
-      run_leaves_global(tr, d_list, count, in_a, nullptr, 0);
+    if (mode == SS_MODE_LT) {   // semisort<: (key, index) bitonic per CTA in shared memory
+      const size_t sm = leaf_lt_smem_bytes<K, V>();
+      auto kern = k_leaf_lt_smem<K, V>;
+      SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      int per_sm = 0;
+      SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, sm));
+      const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
+      kern<<<grid, kLeafThreads, sm, st>>>(in_a ? A_k : S_k, in_a ? A_v : S_v, A_k, A_v, d_list,
+                                           static_cast<uint32_t>(count), in_a ? 1u : s_ss());
+      check_launch();
+      tr.launched();
+      if (tel) tel->leaves_smem += count;
       return;
     }
     leaf_stats("smem", d_list, count, st);
@@ -333,8 +356,8 @@ struct SortEngine {
     std::vector<Leaf> tiny, small, mid, huge;
     const uint64_t mmax_planned = std::max<uint64_t>(1, std::min<uint64_t>(n, P.base_case_cutoff > 1 ? P.base_case_cutoff - 1 : 1));
     for (const Leaf& l : leaves) {
-      if (l.size <= kLeafWarpMax && mode == SS_MODE_EQ) tiny.push_back(l);
-      else if (l.size <= kLeafSmemMax && mode == SS_MODE_EQ) small.push_back(l);
+      if (l.size <= kLeafWarpMax) tiny.push_back(l);
+      else if (l.size <= kLeafSmemMax) small.push_back(l);
       else if (l.size <= mmax_planned) mid.push_back(l);
       else huge.push_back(l);
     }
@@ -465,7 +488,7 @@ struct SortEngine {
     // children
     tr.begin(kPhChildren);
     SS_CUDA(cudaMemsetAsync(d_misc, 0, 8 * sizeof(uint64_t), st));
-    const LeafClasses lcls{mode == SS_MODE_EQ ? kLeafWarpMax : 0, kLeafSmemMax, P.base_case_cutoff};
+    const LeafClasses lcls{kLeafWarpMax, kLeafSmemMax, P.base_case_cutoff};
     k_children_count<<<nn, 256, 0, st>>>(d_nodes, nn, d_off, stride, P.light_buckets, lcls, d_ccnt);
     check_launch();
     k_children_scan<<<1, 1024, 0, st>>>(d_ccnt, nn, d_misc);
