@@ -444,7 +444,7 @@ def main():
             S.semisort(work, adp, args.mode, params, telemetry=timed_tel)
             out = work
         else:
-            out = dist_semisort(work, adp, telemetry=timed_tel)
+            out = dist_semisort(work, adp, args.mode, telemetry=timed_tel)
         e1.record(st)
         torch.cuda.synchronize()
         barrier()
