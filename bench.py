@@ -55,8 +55,10 @@ def measured_peaks():
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons during the timed region.
 
-    Polls NVML every ~2 ms (a 5-step c2 run is ~130 ms; nvidia-smi at 0.2 s
-    saw one sample), falling back to nvidia-smi when NVML is unavailable.
+    Polls NVML every 25 ms (a 5-step c2 run is ~130 ms; nvidia-smi at 0.2 s
+    saw one sample; NVML at 2 ms contended with the launches of small-kernel
+    workloads for the driver), falling back to nvidia-smi when NVML is
+    unavailable.
     """
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
@@ -70,17 +72,22 @@ class ClockSampler:
         self.samples = []   # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
+        self._nv = self._h = None
+        try:   # NVML set up outside the timed region
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv, self._h = nv, nv.nvmlDeviceGetHandleByIndex(index)
+            self._mx = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self._reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception:
+            self._nv = None
 
-    def _run_nvml(self, nv):
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        while not self._stop.is_set():
-            bits = get_reasons(h)
-            self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx),
-                                 {name for name, bit in self.REASONS if bits & bit}))
-            self._stop.wait(0.002)
+    def _sample_nvml(self):
+        nv, h = self._nv, self._h
+        bits = self._reasons(h)
+        self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), self._mx,
+                             {name for name, bit in self.REASONS if bits & bit}))
 
     def _run_smi(self):
         names = [name for name, _ in self.REASONS]
@@ -98,25 +105,29 @@ class ClockSampler:
             self._stop.wait(0.05)
 
     def _run(self):
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-        except Exception:
+        if self._nv is None:
             return self._run_smi()
-        try:
-            self._run_nvml(nv)
-        except Exception:
-            self._run_smi()
+        while not self._stop.wait(0.025):
+            try:
+                self._sample_nvml()
+            except Exception:
+                return
 
     def __enter__(self):
+        if self._nv is not None:
+            self._sample_nvml()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.01)   # first sample before the timed region
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nv is not None:
+            try:
+                self._sample_nvml()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
