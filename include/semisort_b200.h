@@ -14,7 +14,8 @@
  * ss_last_error() returns a thread-local message for the last failure.
  *
  * Buffers are SoA exactly like the reference RecordArray (records.py:34-132):
- * keys are uint32 or uint64 (key_bytes 4 / 8); values are optional
+ * keys are uint32 or uint64 (key_bytes 4 / 8), and for ss_semisort also
+ * 128-bit (key_bytes 16: (lo, hi) uint64 rows, records.py:8-10); values are optional
  * (value_bytes 0 / 4 / 8 / 16).  All work is stream-ordered on `stream`.
  * Callers own every buffer; scratch comes from a caller-provided workspace
  * (size queries below), so the library never allocates on the hot path.
@@ -98,7 +99,10 @@ uint64_t ss_semisort_workspace_bytes(uint64_t n, uint32_t key_bytes, uint32_t va
                                      const ss_params* params);
 
 /* In place on (keys, values); mode SS_MODE_EQ / SS_MODE_LT; identity != 0
- * selects the identity hash (adapters.py:112-119). */
+ * selects the identity hash (adapters.py:112-119).  key_bytes 16 runs the
+ * UInt128KeyAdapter semantics (adapters.py:147-198): hash mix64(mix64(hi) ^ lo)
+ * (identity: lo), equality on both words, SS_MODE_LT order by (hi, lo);
+ * keys must be 16-byte aligned. */
 int ss_semisort(void* keys, void* values, uint64_t n, uint32_t key_bytes, uint32_t value_bytes,
                 int mode, int identity, const ss_params* params, void* workspace,
                 uint64_t workspace_bytes, ss_telemetry* telemetry, void* stream);

@@ -123,9 +123,30 @@ class OracleTelemetry:
 # --------------------------------------------------------------------------
 
 def key_hash(keys: np.ndarray, identity: bool) -> np.ndarray:
-    """adapters.py:112-116: u64 widening, then mix64 unless identity."""
-    k = np.asarray(keys).astype(np.uint64)
+    """adapters.py:112-116: u64 widening, then mix64 unless identity.
+
+    128-bit keys ((n, 2) u64 rows, column 0 = lo; records.py:8-10) hash as
+    mix64(mix64(hi) ^ lo), or lo in identity mode (adapters.py:155-159).
+    """
+    k = np.asarray(keys)
+    if k.ndim == 2:
+        lo, hi = k[:, 0].astype(np.uint64), k[:, 1].astype(np.uint64)
+        return lo.copy() if identity else mix64_np(mix64_np(hi) ^ lo)
+    k = k.astype(np.uint64)
     return k if identity else mix64_np(k)
+
+
+def _kv(keys: np.ndarray) -> np.ndarray:
+    """1-D view usable for equality / np.unique: 128-bit rows become void16."""
+    k = np.asarray(keys)
+    if k.ndim == 1:
+        return k.astype(np.uint64)
+    return np.ascontiguousarray(k, dtype=np.uint64).view(np.dtype((np.void, 16))).ravel()
+
+
+def _key_obj(row):
+    """Canonical key (adapters.py:161-166): an int, or (lo, hi) for 128-bit."""
+    return (int(row[0]), int(row[1])) if np.ndim(row) else int(row)
 
 
 def light_slice(h: np.ndarray, depth: int, P: OracleParams) -> np.ndarray:
@@ -151,14 +172,14 @@ def sample_heavy(keys: np.ndarray, P: OracleParams, rng_key: int) -> list:
         return []
     pos = np.random.Generator(np.random.Philox(key=rng_key)).integers(0, m, size=draws)
     s = np.asarray(keys)[pos].astype(np.uint64)
-    uniq, first, cnt = np.unique(s, return_index=True, return_counts=True)
+    _, first, cnt = np.unique(_kv(s), return_index=True, return_counts=True)
     keep = cnt >= P.threshold
-    uniq, first, cnt = uniq[keep], first[keep], cnt[keep]
-    if len(uniq) > P.max_heavy:
+    first, cnt = first[keep], cnt[keep]
+    if len(first) > P.max_heavy:
         sel = np.lexsort((first, -cnt))[: P.max_heavy]
-        uniq, first = uniq[sel], first[sel]
-    order = np.argsort(first, kind="stable")
-    return [int(k) for k in uniq[order]]
+        first = first[sel]
+    first = np.sort(first)
+    return [_key_obj(s[f]) for f in first]
 
 
 def bucket_ids(keys: np.ndarray, heavy: list, P: OracleParams, depth: int,
@@ -166,7 +187,12 @@ def bucket_ids(keys: np.ndarray, heavy: list, P: OracleParams, depth: int,
     """core.py:169-213: light slice, overridden by heavy id n_L + slot."""
     k = np.asarray(keys).astype(np.uint64)
     ids = light_slice(key_hash(k, identity), depth, P)
-    if heavy:
+    if heavy and k.ndim == 2:   # 128-bit: match row by row (adapters.py:187-191)
+        kv = _kv(k)
+        tv = _kv(np.asarray(heavy, dtype=np.uint64).reshape(-1, 2))
+        for slot in range(len(tv)):
+            ids[kv == tv[slot]] = P.n_light + slot
+    elif heavy:
         table = np.asarray(heavy, dtype=np.uint64)
         order = np.argsort(table, kind="stable")
         st = table[order]
@@ -231,17 +257,21 @@ def eq_leaf_order(keys: np.ndarray, identity: bool) -> np.ndarray:
     m = len(k)
     if m < 2:
         return np.arange(m)
-    uniq, first, inv = np.unique(k, return_index=True, return_inverse=True)
+    uniq, first, inv = np.unique(_kv(k), return_index=True, return_inverse=True)
     cap = 1 << max(1, 2 * m - 1).bit_length()
-    cell = (key_hash(uniq, identity) & np.uint64(cap - 1)).astype(np.int64)
+    cell = (key_hash(k[first], identity) & np.uint64(cap - 1)).astype(np.int64)
     grank = np.empty(len(uniq), dtype=np.int64)
     grank[np.lexsort((first, cell))] = np.arange(len(uniq))
     return np.argsort(grank[inv.reshape(-1)], kind="stable")
 
 
 def lt_leaf_order(keys: np.ndarray) -> np.ndarray:
-    """core.py:425-429 / adapters.py:132-135: stable sort by key."""
-    return np.argsort(np.asarray(keys), kind="stable")
+    """core.py:425-429 / adapters.py:132-135: stable sort by key; 128-bit
+    keys by (hi, lo) (adapters.py:178-182)."""
+    k = np.asarray(keys)
+    if k.ndim == 2:
+        return np.lexsort((k[:, 0], k[:, 1]))
+    return np.argsort(k, kind="stable")
 
 
 # --------------------------------------------------------------------------

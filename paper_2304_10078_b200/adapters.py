@@ -1,11 +1,12 @@
 """Key adapters of the drop-in surface (adapters.py:25-284 of the reference).
 
-The GPU path implements the fixed-width integer adapter: hash =
+The GPU path implements the fixed-width integer adapters: hash =
 mix64(u64(key)) or the identity (adapters.py:112-119), equality on the key
-bits, stable order by key value.  Any adapter whose hash or equality is
-arbitrary Python (a subclass overriding them, 128-bit or byte-view keys)
-cannot run on the device and is rejected with ContractError instead of being
-silently executed on the CPU.
+bits, stable order by key value; and, for semisort only, the 128-bit adapter
+(hash mix64(mix64(hi) ^ lo) or lo, order (hi, lo); adapters.py:147-198).  Any
+adapter whose hash or equality is arbitrary Python (a subclass overriding
+them, byte-view keys) cannot run on the device and is rejected with
+ContractError instead of being silently executed on the CPU.
 """
 
 from __future__ import annotations
@@ -50,13 +51,22 @@ class UIntKeyAdapter(KeyAdapter):
 
 
 class UInt128KeyAdapter(KeyAdapter):
-    """128-bit keys: part of the reference API, not of the GPU hot path."""
+    """128-bit keys as (lo, hi) word pairs (adapters.py:147-198).
+
+    semisort runs them on the device; the aggregation and phase-level entry
+    points stay 32/64-bit and reject them with ContractError.
+    """
 
     key_kind = "u128"
 
     def __init__(self, identity: bool = False, with_lt: bool = True):
         self.identity_mode = identity
         self.has_lt = with_lt
+
+    def hash_scalar(self, key) -> int:
+        lo, hi = key
+        lo &= U64_MASK
+        return lo if self.identity_mode else _mix64(_mix64(hi & U64_MASK) ^ lo)
 
 
 class BytesKeyAdapter(KeyAdapter):
@@ -76,15 +86,18 @@ def adapter_for(data, *, identity: bool = False) -> KeyAdapter:
     return BytesKeyAdapter(getattr(data, "arena", None))
 
 
-def device_identity_flag(adapter: KeyAdapter) -> int:
+def device_identity_flag(adapter: KeyAdapter, allow_u128: bool = False) -> int:
     """1/0 identity mode for a device-executable adapter, else ContractError."""
-    if not isinstance(adapter, UIntKeyAdapter):
+    base = UIntKeyAdapter
+    if allow_u128 and isinstance(adapter, UInt128KeyAdapter):
+        base = UInt128KeyAdapter
+    elif not isinstance(adapter, UIntKeyAdapter):
         raise ContractError(
-            f"{type(adapter).__name__} keys are not supported by the GPU path "
+            f"{type(adapter).__name__} keys are not supported by this GPU entry point "
             "(fixed-width integer keys only)")
     custom = ("hash_scalar", "hash_block", "group_block", "sort_block", "match_packed", "match_rows")
     for cls in type(adapter).__mro__:
-        if cls is UIntKeyAdapter:
+        if cls is base:
             break
         for name in custom:
             if name in cls.__dict__:

@@ -165,10 +165,10 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def _layout(data: RecordArray) -> tuple[int, int]:
+def _layout(data: RecordArray, allow_u128: bool = False) -> tuple[int, int]:
     if not isinstance(data, RecordArray):
         raise ContractError("data must be a paper_2304_10078_b200.RecordArray")
-    if data.key_kind not in ("u32", "u64"):
+    if data.key_kind not in (("u32", "u64", "u128") if allow_u128 else ("u32", "u64")):
         raise ContractError(f"{data.key_kind} keys are not supported by the GPU path")
     vb = data.value_bytes
     if vb not in (0, 4, 8, 16):
@@ -411,8 +411,10 @@ def semisort(data: RecordArray, adapter: KeyAdapter, mode: str = "eq", params: T
         raise ConfigurationError(f"mode must be 'eq' or 'lt', got {mode!r}")
     if mode == "lt" and not adapter.has_lt:
         raise ContractError("mode 'lt' requires an adapter with a less-than test")
-    ident = device_identity_flag(adapter)
-    kb, vb = _layout(data)
+    ident = device_identity_flag(adapter, allow_u128=True)
+    kb, vb = _layout(data, allow_u128=True)
+    if (data.key_kind == "u128") != (adapter.key_kind == "u128"):
+        raise ContractError(f"{type(adapter).__name__} does not match {data.key_kind} keys")
     n = len(data)
     params = _check_params(params, n)
     tel = telemetry if telemetry is not None else Telemetry()

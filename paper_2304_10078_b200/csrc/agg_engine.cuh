@@ -400,7 +400,7 @@ struct AggEngine {
     d_misc = a.take<uint64_t>(8);
     d_leaf_s = a.take<Leaf>(max_leaves);
     d_leaf_g = a.take<Leaf>(max_leaves);
-    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * (2 * s_cap + 2 * pow2_ge(s_cap)));
+    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * sample_scratch_words(s_cap, 8));
     d_leafscr = a.take<uint32_t>(static_cast<uint64_t>(leafg_grid) * leafg_words);
     d_HS = a.take<unsigned long long>(max_rows * mh);
     d_ntot = a.take<uint64_t>(max_nodes);

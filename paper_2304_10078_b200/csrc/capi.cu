@@ -35,6 +35,20 @@ void dispatch_kv(uint32_t kb, uint32_t vb, F&& f) {
   }
 }
 
+// dispatch_kv plus 128-bit keys (records.py:8-10): the semisort entry points
+// only; aggregation and the phase-level API stay 32/64-bit.
+template <typename F>
+void dispatch_sort(uint32_t kb, uint32_t vb, F&& f) {
+  check_widths(kb, vb, true);
+  if (kb != 16) return dispatch_kv(kb, vb, f);
+  switch (vb) {
+    case 0: f.template operator()<U128, NoVal>(); return;
+    case 4: f.template operator()<U128, uint32_t>(); return;
+    case 8: f.template operator()<U128, uint64_t>(); return;
+    default: f.template operator()<U128, V16>(); return;
+  }
+}
+
 template <typename F>
 void dispatch_k(uint32_t kb, F&& f) {
   if (kb == 8) f.template operator()<uint64_t>();
@@ -81,7 +95,7 @@ struct PhasePlan {
     leaf_words_n = std::max(leaf_words(std::max<uint64_t>(n, 1), false), lt_leaf_words(n, key_bytes));
     d_leafscr = a.take<uint32_t>(leaf_words_n);
     s_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, P.sample_count));
-    d_samp = a.take<uint64_t>(2 * s_cap + 2 * pow2_ge(s_cap));
+    d_samp = a.take<uint64_t>(sample_scratch_words(s_cap, 8));
     d_ids = a.take<uint16_t>(n);
   }
 
@@ -183,7 +197,7 @@ uint64_t ss_semisort_workspace_bytes(uint64_t n, uint32_t key_bytes, uint32_t va
   uint64_t out = 0;
   int rc = guarded([&] {
     Params P = to_params(params, n, false);
-    dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
+    dispatch_sort(key_bytes, value_bytes, [&]<typename K, typename V>() {
       SortEngine<K, V> e{};
       e.n = n;
       e.P = P;
@@ -203,7 +217,7 @@ int ss_semisort(void* keys, void* values, uint64_t n, uint32_t key_bytes, uint32
     Params P = to_params(params, n, true);
     if (value_bytes && !values && n) throw Fail(SS_ERR_CONTRACT, "values pointer is NULL");
     reset_tel(telemetry);
-    dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
+    dispatch_sort(key_bytes, value_bytes, [&]<typename K, typename V>() {
       SortEngine<K, V> e{};
       e.A_k = static_cast<K*>(keys);
       e.A_v = static_cast<V*>(values);

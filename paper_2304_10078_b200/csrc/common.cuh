@@ -47,18 +47,58 @@ __device__ __forceinline__ void store_val(V* p, uint64_t i, const V& v) { p[i] =
 template <>
 __device__ __forceinline__ void store_val<NoVal>(NoVal*, uint64_t, const NoVal&) {}
 
+// 128-bit key (UInt128KeyAdapter, adapters.py:147-197): (lo, hi) words;
+// equality on both words, order lexicographic by (hi, lo) (np.lexsort((lo,
+// hi)), adapters.py:186-190).
+struct alignas(16) U128 {
+  uint64_t lo, hi;
+  U128() = default;
+  __host__ __device__ explicit constexpr U128(uint64_t v) : lo(v), hi(0) {}   // K(0) padding
+  __host__ __device__ constexpr U128(uint64_t l, uint64_t h) : lo(l), hi(h) {}
+};
+__host__ __device__ __forceinline__ bool operator==(const U128& a, const U128& b) { return a.lo == b.lo && a.hi == b.hi; }
+__host__ __device__ __forceinline__ bool operator!=(const U128& a, const U128& b) { return !(a == b); }
+__host__ __device__ __forceinline__ bool operator<(const U128& a, const U128& b) {
+  return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
+}
+__host__ __device__ __forceinline__ bool operator>(const U128& a, const U128& b) { return b < a; }
+
+// How a key is stored in heavy tables and sample buffers: u32 keys widen to
+// u64 (adapters.py:113), u64 and U128 keys are kept as they are.
+template <typename K> struct KeyTraits {
+  using Store = uint64_t;
+  __host__ __device__ static uint64_t widen(K k) { return static_cast<uint64_t>(k); }
+};
+template <> struct KeyTraits<U128> {
+  using Store = U128;
+  __host__ __device__ static U128 widen(U128 k) { return k; }
+};
+template <typename K> using KeyStore = typename KeyTraits<K>::Store;
+
+__host__ __device__ __forceinline__ uint64_t low_word(uint64_t k) { return k; }
+__host__ __device__ __forceinline__ uint64_t low_word(const U128& k) { return k.lo; }
+
 // Read-only streaming load of one key.
 template <typename K>
 __device__ __forceinline__ K ldg_key(const K* p, uint64_t i) { return __ldg(p + i); }
+template <>
+__device__ __forceinline__ U128 ldg_key<U128>(const U128* p, uint64_t i) {
+  const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(p) + i);
+  return U128(w.x, w.y);
+}
 
 // ---------------------------------------------------------------------------
 // key hash and light ids
 // ---------------------------------------------------------------------------
 
 template <typename K>
-__device__ __forceinline__ uint64_t key_hash(K key, bool identity) {
+__host__ __device__ __forceinline__ uint64_t key_hash(K key, bool identity) {
   uint64_t k = static_cast<uint64_t>(key);   // u32 keys widen (adapters.py:113)
   return identity ? k : mix64(k);
+}
+// 128-bit keys: mix64(mix64(hi) ^ lo), identity: lo (adapters.py:158-168)
+__host__ __device__ __forceinline__ uint64_t key_hash(const U128& key, bool identity) {
+  return identity ? key.lo : mix64(mix64(key.hi) ^ key.lo);
 }
 
 // Per-node light-id slice: rnd, slot = divmod(depth, rounds) (core.py:146-151).
@@ -92,29 +132,34 @@ struct LightCfg {
 constexpr int kHeavySlots = 1024;   // >= 2 * max_heavy (500); power of two
 constexpr int kMaxHeavyDevice = 512;
 
-// Open-addressing table keyed by the heavy key; the home slot is the top 10
-// bits of the key's (mixed) hash, and a 1024-bit home bitmap lets the
-// common light record leave after one shared-memory word test.
-struct HeavySmem {
-  uint64_t keys[kHeavySlots];
+// Open-addressing table keyed by the heavy key (stored as KeyStore<K>); the
+// home slot is the top 10 bits of the key's (mixed) hash, and a 1024-bit
+// home bitmap lets the common light record leave after one shared-memory
+// word test.
+template <typename S>
+struct HeavySmemT {
+  S keys[kHeavySlots];
   unsigned short ids[kHeavySlots];
   uint32_t home_bits[kHeavySlots / 32];
 };
+using HeavySmem = HeavySmemT<uint64_t>;
 
-// 64-bit hash used for the table home slot (mix64 for identity keys too).
-__device__ __forceinline__ uint64_t heavy_hash(uint64_t key, uint64_t h, bool identity) {
-  return identity ? key * kGamma : h;
+// 64-bit hash used for the table home slot (mixed for identity keys too).
+template <typename S>
+__device__ __forceinline__ uint64_t heavy_hash(const S& key, uint64_t h, bool identity) {
+  return identity ? low_word(key) * kGamma : h;
 }
 __device__ __forceinline__ uint32_t heavy_home_of(uint64_t hh) { return static_cast<uint32_t>(hh >> 54); }
 
 // Cooperative parallel build; caller must __syncthreads() afterwards.
-__device__ __forceinline__ void heavy_build(HeavySmem& t, const uint64_t* heavy, uint32_t n_heavy, bool identity) {
+template <typename S>
+__device__ __forceinline__ void heavy_build(HeavySmemT<S>& t, const S* heavy, uint32_t n_heavy, bool identity) {
   for (int s = threadIdx.x; s < kHeavySlots; s += blockDim.x) t.ids[s] = 0xFFFF;
   for (int s = threadIdx.x; s < kHeavySlots / 32; s += blockDim.x) t.home_bits[s] = 0;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n_heavy; i += blockDim.x) {
-    const uint64_t k = heavy[i];
-    const uint32_t home = heavy_home_of(heavy_hash(k, identity ? k : mix64(k), identity));
+    const S k = heavy[i];
+    const uint32_t home = heavy_home_of(heavy_hash(k, key_hash(k, identity), identity));
     atomicOr(&t.home_bits[home >> 5], 1u << (home & 31));
     uint32_t s = home;
     while (atomicCAS(&t.ids[s], static_cast<unsigned short>(0xFFFF), static_cast<unsigned short>(i)) != 0xFFFF)
@@ -124,7 +169,8 @@ __device__ __forceinline__ void heavy_build(HeavySmem& t, const uint64_t* heavy,
 }
 
 // Returns the heavy slot of key (with 64-bit hash h) or -1.
-__device__ __forceinline__ int heavy_find(const HeavySmem& t, uint64_t key, uint64_t h, bool identity) {
+template <typename S>
+__device__ __forceinline__ int heavy_find(const HeavySmemT<S>& t, const S& key, uint64_t h, bool identity) {
   uint32_t s = heavy_home_of(heavy_hash(key, h, identity));
   if (!(t.home_bits[s >> 5] & (1u << (s & 31)))) return -1;
   while (true) {
@@ -137,10 +183,10 @@ __device__ __forceinline__ int heavy_find(const HeavySmem& t, uint64_t key, uint
 
 // Bucket id of a key at a node: heavy -> n_light + slot, else the light slice.
 template <typename K>
-__device__ __forceinline__ uint32_t bucket_of(K key, const HeavySmem& t, uint32_t n_heavy,
+__device__ __forceinline__ uint32_t bucket_of(K key, const HeavySmemT<KeyStore<K>>& t, uint32_t n_heavy,
                                               const LightCfg& lc, bool identity, uint32_t n_light) {
-  const uint64_t k = static_cast<uint64_t>(key);
-  const uint64_t h = identity ? k : mix64(k);
+  const KeyStore<K> k = KeyTraits<K>::widen(key);
+  const uint64_t h = key_hash(k, identity);
   if (n_heavy) {
     int hv = heavy_find(t, k, h, identity);
     if (hv >= 0) return n_light + static_cast<uint32_t>(hv);

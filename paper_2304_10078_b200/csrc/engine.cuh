@@ -87,8 +87,9 @@ inline Params to_params(const ss_params* p, uint64_t n, bool check_n) {
   return P;
 }
 
-inline void check_widths(uint32_t kb, uint32_t vb) {
-  if (kb != 4 && kb != 8) throw Fail(SS_ERR_CONTRACT, "key_bytes must be 4 or 8");
+inline void check_widths(uint32_t kb, uint32_t vb, bool allow_u128 = false) {
+  if (kb != 4 && kb != 8 && !(allow_u128 && kb == 16))
+    throw Fail(SS_ERR_CONTRACT, allow_u128 ? "key_bytes must be 4, 8 or 16" : "key_bytes must be 4 or 8");
   if (vb != 0 && vb != 4 && vb != 8 && vb != 16)
     throw Fail(SS_ERR_CONTRACT, "value_bytes must be 0, 4, 8 or 16");
 }

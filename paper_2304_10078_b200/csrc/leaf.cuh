@@ -302,7 +302,7 @@ __device__ __forceinline__ void leaf_stage(K* S_k, V* S_v, K* A_k, V* A_v, const
         const K k = base[2 * i];
         const K v = base[2 * i + 1];
         A_k[lf.lo + i] = k;
-        if constexpr (kHasV) A_v[lf.lo + i] = static_cast<V>(v);
+        if constexpr (std::is_same_v<K, V>) A_v[lf.lo + i] = v;   // pairs imply K == V
       }
       __syncthreads();
     }

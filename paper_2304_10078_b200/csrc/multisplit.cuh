@@ -29,18 +29,20 @@ namespace ss {
 // ---------------------------------------------------------------------------
 
 // Semisort / aggregate buckets: heavy table lookup, else the light slice.
-struct KeyBuckets {
-  const uint64_t* heavy;   // [node][max_heavy]
+// S: heavy-key storage (KeyStore<K>: u64 for u32/u64 keys, U128).
+template <typename S = uint64_t>
+struct KeyBucketsT {
+  const S* heavy;   // [node][max_heavy]
   uint32_t max_heavy;
   uint32_t n_light;
   uint32_t light_bits;
   uint32_t identity;
   // per node, set by prepare()
-  HeavySmem* tab;
+  HeavySmemT<S>* tab;
   LightCfg lc;
   uint32_t n_heavy;
 
-  __device__ __forceinline__ void prepare(const Node& nd, uint32_t node_idx, HeavySmem* t) {
+  __device__ __forceinline__ void prepare(const Node& nd, uint32_t node_idx, HeavySmemT<S>* t) {
     tab = t;
     n_heavy = nd.n_heavy;
     lc = LightCfg::make(nd.depth, light_bits, n_light);
@@ -54,24 +56,26 @@ struct KeyBuckets {
   }
   // the kernel's own __shared__ table: no generic-to-shared conversions
   template <typename K>
-  __device__ __forceinline__ uint32_t operator()(K key, uint64_t, const HeavySmem& t) const {
+  __device__ __forceinline__ uint32_t operator()(K key, uint64_t, const HeavySmemT<S>& t) const {
     return bucket_of(key, t, n_heavy, lc, identity != 0, n_light);
   }
 };
+using KeyBuckets = KeyBucketsT<uint64_t>;
 
 // Precomputed ids (the reference's _counts_from_ids / _distribute_ids).
 struct IdBuckets {
   const int32_t* ids;      // indexed by absolute source position
   uint32_t nb;
-  __device__ __forceinline__ void prepare(const Node&, uint32_t, HeavySmem*) { __syncthreads(); }
+  template <typename T>
+  __device__ __forceinline__ void prepare(const Node&, uint32_t, T*) { __syncthreads(); }
   __device__ __forceinline__ uint32_t n_buckets() const { return nb; }
   __device__ __forceinline__ uint32_t first_hot() const { return nb; }
   template <typename K>
   __device__ __forceinline__ uint32_t operator()(K, uint64_t pos) const {
     return static_cast<uint32_t>(ids[pos]);
   }
-  template <typename K>
-  __device__ __forceinline__ uint32_t operator()(K k, uint64_t pos, const HeavySmem&) const {
+  template <typename K, typename T>
+  __device__ __forceinline__ uint32_t operator()(K k, uint64_t pos, const T&) const {
     return (*this)(k, pos);
   }
 };
@@ -97,7 +101,7 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
         const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, BF bf,
         uint16_t* __restrict__ ids_out, uint32_t kstride = 1) {   // kstride 2: pair scratch layout
   extern __shared__ __align__(16) uint32_t cnt[];
-  __shared__ HeavySmem tab;
+  __shared__ HeavySmemT<KeyStore<K>> tab;
   for (uint32_t wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
     const Work wk = work[wi];
     const Node nd = nodes[wk.node];
@@ -117,7 +121,7 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
       for (uint32_t base = 0; base < full; base += kBatch) {
         K keys[kCountItems];
 #pragma unroll
-        for (int k = 0; k < kCountItems; ++k) keys[k] = __ldg(ws + (base + k * kCountThreads + threadIdx.x) * kstride);
+        for (int k = 0; k < kCountItems; ++k) keys[k] = ldg_key(ws, (base + k * kCountThreads + threadIdx.x) * kstride);
 #pragma unroll
         for (int k = 0; k < kCountItems; ++k) {
           const uint32_t i = base + k * kCountThreads + threadIdx.x;
@@ -134,7 +138,7 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
-        keys[k] = i < len ? __ldg(ws + i * kstride) : K(0);
+        keys[k] = i < len ? ldg_key(ws, i * kstride) : K(0);
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
@@ -325,7 +329,7 @@ __device__ __forceinline__ void fill_span(K* __restrict__ dst, uint64_t lo, uint
 template <typename K, typename V>
 __global__ void k_copy_heavy_fill(K* __restrict__ dk, const V* __restrict__ sv, V* __restrict__ dv,
                                   const Node* __restrict__ nodes, uint32_t n_nodes, const uint64_t* __restrict__ off,
-                                  uint32_t stride, uint32_t n_light, const uint64_t* __restrict__ heavy, uint32_t mh,
+                                  uint32_t stride, uint32_t n_light, const KeyStore<K>* __restrict__ heavy, uint32_t mh,
                                   int pairs = 0) {   // pairs: S is the pair layout (heavy values at words h0 + p)
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   __shared__ uint32_t s_t0;

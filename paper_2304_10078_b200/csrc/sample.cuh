@@ -61,25 +61,31 @@ template <> struct Entry<unsigned long long> {
   static __device__ __forceinline__ uint32_t count(unsigned long long e) { return static_cast<uint32_t>(e); }
 };
 
-template <typename E>
-__device__ void sample_table_insert(E* tab, uint32_t cap, const uint64_t* samp, uint32_t draws) {
+// Lanes of `act` holding the same key (both words for 128-bit keys).
+__device__ __forceinline__ uint32_t match_key(uint32_t act, uint64_t key) { return __match_any_sync(act, key); }
+__device__ __forceinline__ uint32_t match_key(uint32_t act, const U128& key) {
+  return __match_any_sync(act, key.lo) & __match_any_sync(act, key.hi);
+}
+
+template <typename E, typename S>
+__device__ void sample_table_insert(E* tab, uint32_t cap, const S* samp, uint32_t draws) {
   using X = Entry<E>;
   const uint32_t mask = cap - 1;
   for (uint32_t base = 0; base < draws; base += blockDim.x) {
     uint32_t s = base + threadIdx.x;
     bool valid = s < draws;
-    uint64_t key = valid ? samp[s] : 0;
+    const S key = valid ? samp[s] : S(0);
     // lanes holding the same key aggregate; the lowest lane has the
     // smallest stream position
     uint32_t act = __ballot_sync(0xffffffffu, valid);
     if (!valid) continue;
-    uint32_t peers = __match_any_sync(act, key);
+    uint32_t peers = match_key(act, key);
     if (lane_id() != __ffs(peers) - 1) continue;
     uint32_t c = __popc(peers);
     // probe start from the top bits of a multiplicative hash of the folded
     // mix: a node's keys share the low hash bits its ancestors bucketed on,
     // so `mix64(key) & mask` would start every probe in a few slots
-    const uint64_t h = mix64(key);
+    const uint64_t h = key_hash(key, false);
     uint32_t slot = (static_cast<uint32_t>(h ^ (h >> 32)) * 0x9E3779B1u) >> (32 - (31 - __clz(cap)));
     while (true) {
       E old = tab[slot];
@@ -103,21 +109,30 @@ __device__ void sample_table_insert(E* tab, uint32_t cap, const uint64_t* samp, 
   }
 }
 
-// One CTA per node (grid-strided over nodes).  `scratch` holds, per CTA,
-// [samples u64 x s_cap][candidates u64 x s_cap][global table u64 x 2*pow2(s_cap)].
+// Per-CTA scratch words (u64): samples (KeyStore x s_cap), candidates
+// (s_cap) and the global-memory fallback table (2 * pow2(s_cap)).
+__host__ __device__ inline uint64_t sample_scratch_words(uint64_t s_cap, uint32_t key_store_bytes) {
+  uint64_t p = 1;
+  while (p < s_cap) p <<= 1;
+  return s_cap * (key_store_bytes / 8) + s_cap + 2 * p;
+}
+
+// One CTA per node (grid-strided over nodes); `scratch` as above.
 template <typename K>
 __global__ void __launch_bounds__(kSampleThreads)
 k_sample(const K* __restrict__ src, Node* __restrict__ nodes, uint32_t n_nodes,
-         uint64_t* __restrict__ heavy_out, uint64_t* __restrict__ scratch,
+         KeyStore<K>* __restrict__ heavy_out, uint64_t* __restrict__ scratch,
          uint64_t s_cap, Params P, int use_fixed_key, uint64_t fixed_key, uint32_t kstride = 1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t red[33];
   __shared__ uint32_t n_cand;
   uint32_t* stab = reinterpret_cast<uint32_t*>(smem_raw);
-  uint64_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * (2 * s_cap + 2 * pow2_at_least(static_cast<uint32_t>(s_cap)));
-  uint64_t* samp = mine;
-  uint64_t* cand = mine + s_cap;
-  unsigned long long* gtab = reinterpret_cast<unsigned long long*>(mine + 2 * s_cap);
+  using S = KeyStore<K>;
+  constexpr uint32_t kSW = sizeof(S) / 8;
+  uint64_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * sample_scratch_words(s_cap, sizeof(S));
+  S* samp = reinterpret_cast<S*>(mine);
+  uint64_t* cand = mine + kSW * s_cap;
+  unsigned long long* gtab = reinterpret_cast<unsigned long long*>(cand + s_cap);
 
   for (uint32_t j = blockIdx.x; j < n_nodes; j += gridDim.x) {
     const uint64_t lo = nodes[j].lo, m = nodes[j].size;
@@ -166,7 +181,7 @@ k_sample(const K* __restrict__ src, Node* __restrict__ nodes, uint32_t n_nodes,
       uint64_t at = accepted + block_excl_scan<uint64_t>(mine_cnt, red, total);
       for (int w = 0; w < 8; ++w) {
         if (!(flags >> w & 1)) continue;
-        if (at < draws) samp[at] = static_cast<uint64_t>(src[(lo + pos[w]) * kstride]);   // 2: pair layout
+        if (at < draws) samp[at] = static_cast<S>(src[(lo + pos[w]) * kstride]);   // 2: pair layout
         ++at;
       }
       accepted += total;

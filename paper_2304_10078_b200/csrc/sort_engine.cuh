@@ -205,7 +205,7 @@ struct SortEngine {
   V* heavy_src() const { return aos ? reinterpret_cast<V*>(S_k) : S_v; }
   Node* d_nodes = nullptr;
   Node* d_next = nullptr;
-  uint64_t* d_heavy = nullptr;
+  KeyStore<K>* d_heavy = nullptr;
   Work* d_work = nullptr;
   uint32_t* d_grp_node = nullptr;
   uint32_t* d_C = nullptr;
@@ -246,7 +246,7 @@ struct SortEngine {
     }
     d_nodes = a.take<Node>(max_nodes);
     d_next = a.take<Node>(max_nodes);
-    d_heavy = a.take<uint64_t>(max_nodes * std::max<uint32_t>(P.max_heavy, 1));
+    d_heavy = a.take<KeyStore<K>>(max_nodes * std::max<uint32_t>(P.max_heavy, 1));
     d_work = a.take<Work>(max_rows);
     d_grp_node = a.take<uint32_t>(max_grps);
     d_C = a.take<uint32_t>(max_rows * stride);
@@ -259,7 +259,7 @@ struct SortEngine {
     d_leaf_w = a.take<Leaf>(max_leaves);
     d_leaf_s = a.take<Leaf>(max_leaves);
     d_leaf_g = a.take<Leaf>(max_leaves);
-    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * (2 * s_cap + 2 * pow2_ge(s_cap)));
+    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * sample_scratch_words(s_cap, sizeof(KeyStore<K>)));
     d_leafscr = a.take<uint32_t>(static_cast<uint64_t>(leafg_grid) * leafg_words);
     d_ids = a.take<uint16_t>(n);
   }
@@ -437,7 +437,8 @@ struct SortEngine {
     check_launch();
     tr.launched();
 
-    KeyBuckets bf{};
+    using BF = KeyBucketsT<KeyStore<K>>;
+    BF bf{};
     bf.heavy = d_heavy;
     bf.max_heavy = std::max<uint32_t>(P.max_heavy, 1);
     bf.n_light = P.light_buckets;
@@ -446,7 +447,7 @@ struct SortEngine {
 
     // counting matrix
     tr.begin(kPhCount);
-    k_count<K, KeyBuckets><<<nwork, kCountThreads, stride * 4, st>>>(sk, d_work, nwork, d_nodes, d_C, stride, bf,
+    k_count<K, BF><<<nwork, kCountThreads, stride * 4, st>>>(sk, d_work, nwork, d_nodes, d_C, stride, bf,
                                                                      d_ids, kss);
     check_launch();
     tr.launched();

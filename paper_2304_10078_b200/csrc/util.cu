@@ -188,15 +188,16 @@ __global__ void k_count_distinct(const K* __restrict__ keys, uint64_t n, uint64_
 struct PartBuckets {
   uint32_t shift;   // 64 - log2(parts); 64 means a single part
   uint32_t nb;
-  __device__ __forceinline__ void prepare(const Node&, uint32_t, HeavySmem*) { __syncthreads(); }
+  template <typename T>
+  __device__ __forceinline__ void prepare(const Node&, uint32_t, T*) { __syncthreads(); }
   __device__ __forceinline__ uint32_t n_buckets() const { return nb; }
   __device__ __forceinline__ uint32_t first_hot() const { return nb; }
   template <typename K>
   __device__ __forceinline__ uint32_t operator()(K key, uint64_t) const {
     return shift >= 64 ? 0u : static_cast<uint32_t>(mix64(static_cast<uint64_t>(key)) >> shift);
   }
-  template <typename K>
-  __device__ __forceinline__ uint32_t operator()(K key, uint64_t pos, const HeavySmem&) const {
+  template <typename K, typename T>
+  __device__ __forceinline__ uint32_t operator()(K key, uint64_t pos, const T&) const {
     return (*this)(key, pos);
   }
 };
