@@ -233,6 +233,17 @@ int ss_csr_from_edges(uint64_t n_vertices, uint64_t m, const uint32_t* sources, 
                       uint64_t* out_offsets, uint32_t* out_targets, const ss_params* params,
                       void* workspace, uint64_t workspace_bytes, ss_telemetry* telemetry, void* stream);
 
+/* ---- record-dump rows (records.py:149-202) --------------------------------
+ * A record dump ("SSR1" header, then n packed little-endian rows of
+ * key_bytes + value_bytes, key first) is split into / packed from SoA device
+ * columns.  rows, keys, values are device buffers, 4-byte aligned; key_bytes
+ * 4 / 8 / 16, value_bytes a multiple of 4 (0 = no values).  The header itself
+ * is parsed by the caller (write_records / read_records). */
+int ss_records_unpack(const void* rows, uint64_t n, uint32_t key_bytes, uint32_t value_bytes, void* keys,
+                      void* values, void* stream);
+int ss_records_pack(const void* keys, const void* values, uint64_t n, uint32_t key_bytes, uint32_t value_bytes,
+                    void* rows, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,8 @@ _SIGS = {
                                  C.POINTER(SSTelemetry), vp]),
     "ss_csr_from_edges": (i32, [u64, u64, vp, vp, vp, vp, C.POINTER(SSParams), vp, u64,
                                 C.POINTER(SSTelemetry), vp]),
+    "ss_records_unpack": (i32, [vp, u64, u32, u32, vp, vp, vp]),
+    "ss_records_pack": (i32, [vp, vp, u64, u32, u32, vp, vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -9,6 +9,9 @@ data enters the drop-in path.  Views never copy.
 
 from __future__ import annotations
 
+import os
+import struct
+
 import numpy as np
 import torch
 
@@ -184,3 +187,81 @@ class RecordArray:
             return True
         return self.values.dtype == other.values.dtype and torch.equal(
             signed_view(self.values), signed_view(other.values.to(self.device)))
+
+
+# -- binary record dump (records.py:149-202) ----------------------------------
+# 16-byte header: magic "SSR1", key_width u16, value_width u16, n u64 (little
+# endian); then n packed rows, key bytes first.  The payload moves between the
+# file and HBM untouched (one pinned staging buffer, one copy each way); the
+# row <-> column split runs on the device (ss_records_unpack / _pack).
+
+DUMP_MAGIC = b"SSR1"
+_HEADER = struct.Struct("<HHQ")
+
+
+def _payload_stage(nbytes: int) -> torch.Tensor:
+    t = torch.empty(max(nbytes, 1), dtype=torch.uint8)
+    return t.pin_memory() if torch.cuda.is_available() else t
+
+
+def write_records(path, data: "RecordArray") -> None:
+    """records.py:152-169: same header and row bytes as the reference."""
+    from . import _lib
+    if data.key_kind == "bytes":
+        raise InputFormatError("byte-view records cannot be dumped (arena-backed)")
+    n = len(data)
+    kb = data.key_bytes
+    vb = data.value_bytes
+    header = DUMP_MAGIC + _HEADER.pack(data.key_width, vb * 8, n)
+    row = kb + vb
+    dev = data.device
+    stage = _payload_stage(n * row)
+    if n:
+        rows = torch.empty(n * row, dtype=torch.uint8, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().ss_records_pack(data.keys.data_ptr(),
+                                              None if data.values is None else data.values.data_ptr(),
+                                              n, kb, vb, rows.data_ptr(), st))
+        stage[: n * row].copy_(rows)
+    with open(path, "wb") as fh:
+        fh.write(header)
+        if n:
+            fh.write(memoryview(stage[: n * row].numpy()))
+
+
+def read_records(path, device=None) -> "RecordArray":
+    """records.py:172-202: same checks and errors; columns land on the GPU."""
+    from . import _lib
+    with open(path, "rb") as fh:
+        header = fh.read(16)
+        if len(header) != 16 or header[:4] != DUMP_MAGIC:
+            raise InputFormatError(f"{path}: not a record dump")
+        key_width, value_width, n = _HEADER.unpack(header[4:])
+        row = (key_width + value_width) // 8
+        size = os.fstat(fh.fileno()).st_size - 16
+        if key_width not in (32, 64, 128) or size != n * row:
+            raise InputFormatError(f"{path}: corrupt record dump header")
+        if value_width not in (0, 32) and value_width % 64:
+            raise InputFormatError(f"{path}: value width {value_width} is not 32 or a multiple of 64")
+        stage = _payload_stage(n * row)
+        if n and fh.readinto(memoryview(stage[: n * row].numpy())) != n * row:
+            raise InputFormatError(f"{path}: truncated record dump")
+    dev = device or default_device()
+    kind = {32: "u32", 64: "u64", 128: "u128"}[key_width]
+    kshape = (n, 2) if key_width == 128 else (n,)
+    keys = torch.empty(kshape, dtype=torch.uint32 if key_width == 32 else torch.uint64, device=dev)
+    values = None
+    if value_width == 32:
+        values = torch.empty(n, dtype=torch.uint32, device=dev)
+    elif value_width == 64:
+        values = torch.empty(n, dtype=torch.uint64, device=dev)
+    elif value_width:
+        values = torch.empty((n, value_width // 64), dtype=torch.uint64, device=dev)
+    if n:
+        rows = stage[: n * row].to(dev, non_blocking=True)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().ss_records_unpack(rows.data_ptr(), n, key_width // 8, value_width // 8,
+                                                keys.data_ptr(), None if values is None else values.data_ptr(),
+                                                st))
+        torch.cuda.current_stream(dev).synchronize()   # the staging buffer is reused by the caller's GC
+    return RecordArray(keys, values, kind)

@@ -76,6 +76,11 @@ def _is_index_column(values: torch.Tensor | None) -> bool:
     return bool(torch.equal(signed_view(values).to(torch.int64), ar))
 
 
+def _flat_keys(k: np.ndarray) -> np.ndarray:
+    """128-bit (n, 2) rows as one comparable void16 column."""
+    return k if k.ndim == 1 else np.ascontiguousarray(k).view(np.dtype((np.void, 16))).ravel()
+
+
 def validate_semisort(input_data: RecordArray, output_data: RecordArray, adapter=None) -> ValidationReport:
     n = len(input_data)
     if len(output_data) != n:
@@ -85,7 +90,7 @@ def validate_semisort(input_data: RecordArray, output_data: RecordArray, adapter
     if input_data.key_kind in ("u32", "u64") and _is_index_column(input_data.values):
         return validate_indexed(input_data.keys, output_data.keys, output_data.values)
     # definition-level host check (checker only)
-    ki, ko = input_data.keys_host(), output_data.keys_host()
+    ki, ko = _flat_keys(input_data.keys_host()), _flat_keys(output_data.keys_host())
     brk = np.ones(n, dtype=bool)
     brk[1:] = ko[1:] != ko[:-1]
     contiguous = len(np.unique(ko[brk])) == int(brk.sum())
