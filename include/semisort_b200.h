@@ -85,6 +85,7 @@ typedef struct ss_telemetry {
   uint64_t levels;
   uint64_t leaves_smem;
   uint64_t leaves_global;
+  uint64_t nodes_folded;   /* aggregation nodes reduced in one pass (node_fold.cuh) */
   int32_t timing;
   int32_t reserved;
   double phase_ms[8];

@@ -54,6 +54,7 @@ class Telemetry:
     levels: int = 0
     leaves_smem: int = 0
     leaves_global: int = 0
+    nodes_folded: int = 0
     timing: bool = False
     phase_ms: dict = field(default_factory=dict)
 
@@ -84,6 +85,7 @@ class Telemetry:
         self.levels += int(t.levels)
         self.leaves_smem += int(t.leaves_smem)
         self.leaves_global += int(t.leaves_global)
+        self.nodes_folded += int(t.nodes_folded)
         if self.timing:
             for i, name in enumerate(_lib.PHASES):
                 self.phase_ms[name] = self.phase_ms.get(name, 0.0) + float(t.phase_ms[i])

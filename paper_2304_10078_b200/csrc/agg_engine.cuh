@@ -34,6 +34,12 @@ template <typename V> __device__ __forceinline__ uint64_t val_u64(const V& v) { 
 template <> __device__ __forceinline__ uint64_t val_u64<NoVal>(const NoVal&) { return 0; }
 template <> __device__ __forceinline__ uint64_t val_u64<V16>(const V16& v) { return v.lo; }
 
+}  // namespace ss
+
+#include "node_fold.cuh"
+
+namespace ss {
+
 // Counting matrix + per-row heavy partial sums.
 template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kCountThreads)
@@ -358,6 +364,9 @@ struct AggEngine {
   uint64_t* d_ha = nullptr;
   uint64_t* d_hoff = nullptr;
   uint64_t* d_cursor = nullptr;
+  uint32_t* d_ord = nullptr;
+  uint32_t* d_claim = nullptr;
+  uint64_t* d_fstat = nullptr;
 
   void plan(Arena& a) {
     stride = even_stride(P);
@@ -412,9 +421,17 @@ struct AggEngine {
     d_ha = a.take<uint64_t>(max_nodes * mh);
     d_ids = a.take<uint16_t>(n);
     d_hoff = a.take<uint64_t>(max_nodes);
+    d_ord = a.take<uint32_t>(max_nodes);
+    d_claim = a.take<uint32_t>(1);
+    d_fstat = a.take<uint64_t>(2 * max_nodes);
   }
 
   bool sum() const { return kind == SS_AGG_SUM64; }
+  // SS_NODE_FOLD=0 sends every node through the level path (A/B runs, tests)
+  static bool fold_enabled() {
+    const char* e = std::getenv("SS_NODE_FOLD");
+    return !(e && e[0] == '0');
+  }
   // Pair buffers (K == V, sum64, chosen in run()): B holds (key, value)
   // records, element stride 2 -- the light scatter then writes one 16-byte
   // record instead of two partial-sector stores (c3's level 0 is all light).
@@ -480,7 +497,97 @@ struct AggEngine {
     }
   }
 
+  // Node folds (node_fold.cuh): every node of a level below the root whose
+  // light children would all be leaves is reduced in one pass; returns the
+  // nodes that need the regular level path (children >= alpha, or more
+  // distinct keys than the shared-memory table holds).
+  std::vector<Node> fold_nodes(Tracker& tr, std::vector<Node>& cur, int lvl) {
+    const K* sk = B_k[lvl & 1];
+    const V* sv = B_v[lvl & 1];
+    std::vector<Node> rest, fold;
+    for (const Node& nd : cur) (nd.size >> 32 ? rest : fold).push_back(nd);
+    if (fold.empty()) return rest;
+    const uint32_t nn = static_cast<uint32_t>(fold.size());
+    std::vector<uint32_t> ord(nn);
+    std::vector<Leaf> lv(nn);
+    for (uint32_t j = 0; j < nn; ++j) {
+      ord[j] = j;
+      lv[j] = Leaf{fold[j].lo, fold[j].size};
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return fold[a].size > fold[b].size; });
+    SS_CUDA(cudaMemcpyAsync(d_nodes, fold.data(), nn * sizeof(Node), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemcpyAsync(d_ord, ord.data(), nn * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemcpyAsync(d_leaf_g, lv.data(), nn * sizeof(Leaf), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaMemsetAsync(d_claim, 0, sizeof(uint32_t), st));
+
+    tr.begin(kPhSample);
+    SS_CUDA(cudaFuncSetAttribute(k_sample<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSampleSmem)));
+    k_sample<K><<<std::min<uint32_t>(sample_grid, nn), kSampleThreads, kSampleSmem, st>>>(
+        sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0, bss());
+    check_launch();
+    tr.launched();
+
+    KeyBuckets bf{};
+    bf.heavy = d_heavy;
+    bf.max_heavy = mh;
+    bf.n_light = P.light_buckets;
+    bf.light_bits = P.light_bits;
+    bf.identity = identity;
+    tr.begin(kPhLeaves);
+    const size_t sm = node_fold_smem(sizeof(K), sum(), P.light_buckets);
+    auto launch = [&](auto kern) {
+      SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      int dev = 0, sms = 148;
+      SS_CUDA(cudaGetDevice(&dev));
+      SS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      kern<<<std::min<uint32_t>(nn, static_cast<uint32_t>(sms)), kFoldThreads, sm, st>>>(
+          sk, sv, bss(), d_nodes, d_ord, nn, d_claim, bf, P.base_case_cutoff, st_k, st_a, d_G, d_fstat);
+    };
+    if (sum()) launch(k_fold_nodes<K, V, true>);
+    else launch(k_fold_nodes<K, V, false>);
+    check_launch();
+    device_exclusive_scan<uint32_t>(d_G, nn, d_loff, d_part, d_misc + 6, st);
+    k_emit_leaves<K><<<static_cast<uint32_t>(std::min<uint64_t>(cdiv(nn, 8), 148 * 16)), 256, 0, st>>>(
+        d_leaf_g, nn, d_G, d_loff, st_k, st_a, d_out_k, d_out_a, d_cursor);
+    k_bump<<<1, 32, 0, st>>>(d_cursor, d_misc + 6, 0);
+    check_launch();
+    tr.launched(5);
+    tr.end();
+
+    std::vector<uint64_t> fst(2 * static_cast<size_t>(nn));
+    SS_CUDA(cudaMemcpyAsync(fst.data(), d_fstat, fst.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaMemcpyAsync(fold.data(), d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    uint64_t done = 0;
+    for (uint32_t j = 0; j < nn; ++j) {
+      if (fst[2 * j + 1] >> 32) {
+        Node nd = fold[j];
+        nd.n_heavy = 0;
+        rest.push_back(nd);
+        continue;
+      }
+      ++done;
+      if (!tel) continue;
+      const uint64_t kids = fst[2 * j + 1] & 0xFFFFFFFFull;
+      tel->bucket_assignments += fold[j].size;
+      if (lvl <= 64)
+        tel->matrix_cells_by_level[lvl] += cdiv(fold[j].size, P.subarray_len) * (P.light_buckets + fold[j].n_heavy);
+      tel->scratch_moves += fst[2 * j];
+      tel->nodes += kids;
+      if (kids && static_cast<uint64_t>(lvl + 1) > tel->max_depth) tel->max_depth = lvl + 1;
+    }
+    if (tel) tel->nodes_folded += done;
+    return rest;
+  }
+
   std::vector<Node> level(Tracker& tr, std::vector<Node>& cur, int lvl) {
+    if (lvl >= 2 && fold_enabled()) {
+      cur = fold_nodes(tr, cur, lvl);
+      if (cur.empty()) {
+        if (tel) tel->levels += 1;
+        return {};
+      }
+    }
     const K* sk = lvl == 1 ? in_k : B_k[lvl & 1];
     const V* sv = lvl == 1 ? in_v : B_v[lvl & 1];
     K* dk = B_k[(lvl + 1) & 1];

@@ -313,3 +313,64 @@ def test_aggregate_vs_oracle_large(S):
     res = S.histogram(S.RecordArray(keys32), S.UIntKeyAdapter())
     k, v = res.to_numpy()
     assert dict(zip(k.tolist(), v.tolist())) == O.reduce_by_key(keys32, None, "count")
+
+
+# ---- node folds (csrc/node_fold.cuh) ----------------------------------------------
+
+def _fold_cases():
+    rng = np.random.default_rng(21)
+    n = 1 << 20
+    u32max, u64max = np.uint32(0xFFFFFFFF), np.uint64(0xFFFFFFFFFFFFFFFF)
+    zipf = np.minimum(rng.zipf(1.3, n), 10**6).astype(np.uint64)
+    k32 = rng.integers(0, 20000, n).astype(np.uint32)
+    k32[rng.integers(0, n, 5000)] = u32max              # the table's empty marker as a real key
+    k64 = (rng.integers(0, 5000, n).astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15))
+    k64[rng.integers(0, n, 3000)] = u64max
+    wide = rng.integers(0, 2**63, 1 << 22).astype(np.uint64)   # level-2 nodes overflow the table
+    few = rng.integers(0, 1000, n).astype(np.uint64)            # children >= alpha: nodes recurse
+    vals = lambda m: rng.integers(0, 2**64 - 1, m, dtype=np.uint64, endpoint=True)  # noqa: E731
+    return [
+        ("u32_marker", k32, vals(n), {"light_buckets": 64, "base_case_cutoff": 4096}, False),
+        ("u64_marker", k64, vals(n), {"light_buckets": 64, "base_case_cutoff": 4096}, False),
+        ("zipf_heavy", zipf, vals(n), {"light_buckets": 64, "base_case_cutoff": 2048}, False),
+        ("identity", k32.astype(np.uint64), vals(n), {"light_buckets": 32, "base_case_cutoff": 4096}, True),
+        ("wide_overflow", wide, vals(len(wide)), {"light_buckets": 64, "base_case_cutoff": 16384}, False),
+        ("few_recurse", few, vals(n), {"light_buckets": 4, "base_case_cutoff": 16384}, False),
+    ]
+
+
+@pytest.mark.parametrize("case", _fold_cases(), ids=lambda c: c[0])
+def test_node_fold_vs_oracle_and_level_path(S, case, monkeypatch):
+    """Folded nodes give the reference's pairs and Telemetry; the level path
+    (SS_NODE_FOLD=0) gives the same; overflowing / recursing nodes fall back."""
+    name, keys, vals, kw, ident = case
+    n = len(keys)
+    P = S.TuningParams.for_input(n, **kw)
+    OP = O.OracleParams.derive(n, **kw)
+    adp = S.UIntKeyAdapter(identity=ident)
+    for kind, spec in (("count", S.ReduceSpec.counting()), ("sum64", S.ReduceSpec.summing64())):
+        runs = {}
+        for mode in ("1", "0"):
+            monkeypatch.setenv("SS_NODE_FOLD", mode)
+            tel = S.Telemetry()
+            res = S.collect_reduce(S.RecordArray(keys, vals), adp, spec, P, telemetry=tel)
+            runs[mode] = (_sorted_pairs(res), tel)
+        monkeypatch.delenv("SS_NODE_FOLD")
+        pairs, otel = O.collect_reduce(keys, vals if kind == "sum64" else None, OP, kind, identity=ident)
+        ref = np.array(sorted(pairs), dtype=np.uint64).reshape(-1, 2)
+        for mode, (got, tel) in runs.items():
+            assert np.array_equal(got, ref), (name, kind, mode)
+            assert tel.max_depth == otel.max_depth and tel.nodes == otel.nodes, (name, kind, mode)
+            assert tel.scratch_moves == otel.scratch_moves and tel.bucket_assignments == otel.bucket_assignments
+            assert {int(k): v for k, v in tel.matrix_cells_by_level.items()} == \
+                {int(k): v for k, v in otel.matrix_cells_by_level.items()}
+        assert runs["0"][1].nodes_folded == 0
+        if name == "wide_overflow":
+            assert runs["1"][1].nodes_folded == 0, name   # every level-2 node overflowed
+        elif name != "few_recurse":   # (its level-2 nodes recurse; deeper ones may fold)
+            assert runs["1"][1].nodes_folded > 0, name
+        # deterministic output order
+        res2 = S.collect_reduce(S.RecordArray(keys, vals), adp, spec, P)
+        k1, a1 = S.collect_reduce(S.RecordArray(keys, vals), adp, spec, P).to_numpy()
+        k2, a2 = res2.to_numpy()
+        assert np.array_equal(k1, k2) and np.array_equal(a1, a2)
