@@ -200,9 +200,19 @@ k_scan_nodes(const Node* __restrict__ nodes, uint32_t n_nodes, uint64_t* __restr
     const uint32_t per = (cols + blockDim.x - 1) / blockDim.x;
     const uint32_t b0 = min(cols, threadIdx.x * per), b1 = min(cols, b0 + per);
     uint64_t local = 0;
+    constexpr uint32_t kG = 8;   // group loads in flight per thread (the loop is latency-bound)
     for (uint32_t b = b0; b < b1; ++b) {
       uint64_t t = 0;
-      for (uint32_t g = 0; g < nd.n_grps; ++g) t += P[static_cast<uint64_t>(nd.grp_base + g) * stride + b];
+      const uint64_t* p = P + static_cast<uint64_t>(nd.grp_base) * stride + b;
+      uint32_t g = 0;
+      for (; g + kG <= nd.n_grps; g += kG) {
+        uint64_t v[kG];
+#pragma unroll
+        for (uint32_t u = 0; u < kG; ++u) v[u] = p[static_cast<uint64_t>(g + u) * stride];
+#pragma unroll
+        for (uint32_t u = 0; u < kG; ++u) t += v[u];
+      }
+      for (; g < nd.n_grps; ++g) t += p[static_cast<uint64_t>(g) * stride];
       local += t;
     }
     uint64_t total;
@@ -210,10 +220,21 @@ k_scan_nodes(const Node* __restrict__ nodes, uint32_t n_nodes, uint64_t* __restr
     uint64_t* o = off + static_cast<uint64_t>(j) * (stride + 1);
     for (uint32_t b = b0; b < b1; ++b) {
       o[b] = run;
-      for (uint32_t g = 0; g < nd.n_grps; ++g) {
-        uint64_t* p = P + static_cast<uint64_t>(nd.grp_base + g) * stride + b;
-        uint64_t v = *p;
-        *p = run;
+      uint64_t* p = P + static_cast<uint64_t>(nd.grp_base) * stride + b;
+      uint32_t g = 0;
+      for (; g + kG <= nd.n_grps; g += kG) {
+        uint64_t v[kG];
+#pragma unroll
+        for (uint32_t u = 0; u < kG; ++u) v[u] = p[static_cast<uint64_t>(g + u) * stride];
+#pragma unroll
+        for (uint32_t u = 0; u < kG; ++u) {
+          p[static_cast<uint64_t>(g + u) * stride] = run;
+          run += v[u];
+        }
+      }
+      for (; g < nd.n_grps; ++g) {
+        const uint64_t v = p[static_cast<uint64_t>(g) * stride];
+        p[static_cast<uint64_t>(g) * stride] = run;
         run += v;
       }
     }
@@ -280,6 +301,35 @@ __device__ __forceinline__ void copy_span(T* __restrict__ dst, const T* __restri
     }
     for (; i < nv; i += nthreads) d4[i] = s4[i];
     for (uint64_t i = v0 + nv * per + tid; i < hi; i += nthreads) dst[i] = src[i];
+  } else if (sizeof(T) == 4 || sizeof(T) == 8) {
+    // misaligned by a multiple of 4 bytes: aligned 16-byte stores, each fed
+    // by two aligned 16-byte loads funnel-shifted by r words
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(src + lo);
+    uint32_t* dw = reinterpret_cast<uint32_t*>(dst + lo);
+    const uint64_t words = (hi - lo) * (sizeof(T) / 4);
+    uint64_t head = ((16 - (b & 15)) & 15) / 4;
+    if (head > words) head = words;
+    for (uint64_t i = tid; i < head; i += nthreads) dw[i] = sw[i];
+    const uint64_t nv = (words - head) / 4;
+    uint4* d4 = reinterpret_cast<uint4*>(dw + head);
+    const uint32_t* s0 = sw + head;                      // source word of d4[0].x
+    const uint32_t r = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(s0) & 15) / 4);   // 1..3
+    const uint4* s4 = reinterpret_cast<const uint4*>(s0 - r);
+    auto pick = [r](const uint4& x, const uint4& y) {
+      const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+      return r == 1 ? make_uint4(w[1], w[2], w[3], w[4]) : r == 2 ? make_uint4(w[2], w[3], w[4], w[5])
+                                                                  : make_uint4(w[3], w[4], w[5], w[6]);
+    };
+    uint64_t i = tid;
+    for (; i + 3 * nthreads < nv; i += 4 * nthreads) {
+      uint4 o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = pick(__ldcs(s4 + i + u * nthreads), __ldcs(s4 + i + u * nthreads + 1));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d4[i + u * nthreads] = o[u];
+    }
+    for (; i < nv; i += nthreads) d4[i] = pick(__ldcs(s4 + i), __ldcs(s4 + i + 1));
+    for (uint64_t k = head + nv * 4 + tid; k < words; k += nthreads) dw[k] = sw[k];
   } else {
     for (uint64_t i = lo + tid; i < hi; i += nthreads) dst[i] = src[i];
   }
