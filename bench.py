@@ -230,8 +230,12 @@ def agg_main(args):
     peak_gbs, peak_kind = measured_peaks()
     dist_ms = tel.phase_ms.get("distribute", 0.0) / args.steps
     rec_b = c["key_bits"] // 8 + (8 if c["values"] != "none" else 0)
-    moved = tel.bucket_assignments / args.steps
+    # records through the light distribute (folded nodes are read once by k_fold_nodes instead)
+    moved = (tel.bucket_assignments - tel.fold_records) / args.steps
     achieved = (moved * 2 * rec_b) / (dist_ms / 1e3) / 1e9 if dist_ms > 0 else None
+    fold_ms = tel.phase_ms.get("leaves", 0.0) / args.steps
+    folded = tel.fold_records / args.steps
+    fold_gbs = folded * rec_b / (fold_ms / 1e3) / 1e9 if fold_ms > 0 and folded else None
     e2e = None
     if not args.no_e2e:
         hk = torch.empty(n, dtype=src.keys.dtype, pin_memory=True)
@@ -275,7 +279,11 @@ def agg_main(args):
                          "peak_kind": peak_kind,
                          "bytes_model": f"{2 * rec_b} B per bucketed record (read + write {rec_b} B)"},
             "step_roofline": {"bytes_per_record": c["b_alg"], "achieved_gbs": c["b_alg"] * n / (ms / 1e3) / 1e9,
-                              "peak": peak_gbs},
+                              "peak": peak_gbs, "frac_of_nominal_8tbs": c["b_alg"] * n / (ms / 1e3) / NOMINAL_HBM},
+            "fold_roofline": {"kernel": "k_fold_nodes (+ pair emission; the 'leaves' phase)", "records": folded,
+                              "achieved": fold_gbs, "peak": peak_gbs, "unit": "GB/s",
+                              "frac": (fold_gbs / peak_gbs) if fold_gbs else None,
+                              "bytes_model": f"{rec_b} B per folded record (one read)"},
             "phase_ms_per_step": {k: v / args.steps for k, v in tel.phase_ms.items()},
             "gpu_launches": tel.kernel_launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)

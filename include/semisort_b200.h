@@ -86,6 +86,7 @@ typedef struct ss_telemetry {
   uint64_t leaves_smem;
   uint64_t leaves_global;
   uint64_t nodes_folded;   /* aggregation nodes reduced in one pass (node_fold.cuh) */
+  uint64_t fold_records;   /* records of those nodes (read once by the fold) */
   int32_t timing;
   int32_t reserved;
   double phase_ms[8];

@@ -34,7 +34,7 @@ class SSTelemetry(C.Structure):
     _fields_ = [("max_depth", u64), ("nodes", u64), ("scratch_allocations", u64),
                 ("scratch_moves", u64), ("bucket_assignments", u64),
                 ("matrix_cells_by_level", u64 * 65), ("kernel_launches", u64), ("levels", u64),
-                ("leaves_smem", u64), ("leaves_global", u64), ("nodes_folded", u64), ("timing", C.c_int32),
+                ("leaves_smem", u64), ("leaves_global", u64), ("nodes_folded", u64), ("fold_records", u64), ("timing", C.c_int32),
                 ("reserved", C.c_int32), ("phase_ms", C.c_double * 8)]
 
 

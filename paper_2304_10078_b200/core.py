@@ -55,6 +55,7 @@ class Telemetry:
     leaves_smem: int = 0
     leaves_global: int = 0
     nodes_folded: int = 0
+    fold_records: int = 0
     timing: bool = False
     phase_ms: dict = field(default_factory=dict)
 
@@ -86,6 +87,7 @@ class Telemetry:
         self.leaves_smem += int(t.leaves_smem)
         self.leaves_global += int(t.leaves_global)
         self.nodes_folded += int(t.nodes_folded)
+        self.fold_records += int(t.fold_records)
         if self.timing:
             for i, name in enumerate(_lib.PHASES):
                 self.phase_ms[name] = self.phase_ms.get(name, 0.0) + float(t.phase_ms[i])

@@ -568,6 +568,7 @@ struct AggEngine {
       }
       ++done;
       if (!tel) continue;
+      tel->fold_records += fold[j].size;
       const uint64_t kids = fst[2 * j + 1] & 0xFFFFFFFFull;
       tel->bucket_assignments += fold[j].size;
       if (lvl <= 64)
@@ -595,7 +596,10 @@ struct AggEngine {
     const uint32_t nn = static_cast<uint32_t>(cur.size());
     uint64_t R = 0;
     for (auto& nd : cur) R += nd.size;
-    const uint64_t chunk = std::max<uint64_t>(kMinChunk, cdiv(R, kTargetRows));
+    const uint64_t chunk = (std::max<uint64_t>(kMinChunk, cdiv(R, kTargetRows)) + 7) & ~uint64_t(7);   // aligned items
+    uint64_t max_nrows = 0;   // rows per scan group: <= 64 groups per node (see SortEngine::level)
+    for (auto& nd : cur) max_nrows = std::max<uint64_t>(max_nrows, cdiv(nd.size, chunk));
+    const uint32_t rg = static_cast<uint32_t>(std::max<uint64_t>(kRowGroup, cdiv(max_nrows, 64)));
     std::vector<Work> work;
     std::vector<uint32_t> grp_node;
     for (uint32_t j = 0; j < nn; ++j) {
@@ -603,7 +607,7 @@ struct AggEngine {
       nd.row_base = work.size();
       nd.n_rows = static_cast<uint32_t>(cdiv(nd.size, chunk));
       nd.grp_base = static_cast<uint32_t>(grp_node.size());
-      nd.n_grps = static_cast<uint32_t>(cdiv(nd.n_rows, kRowGroup));
+      nd.n_grps = static_cast<uint32_t>(cdiv(nd.n_rows, rg));
       for (uint32_t r = 0; r < nd.n_rows; ++r) {
         Work w;
         w.begin = nd.lo + r * chunk;
@@ -648,11 +652,11 @@ struct AggEngine {
     tr.launched();
 
     tr.begin(kPhScan);
-    k_colsum_groups<uint32_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, stride, P.light_buckets, 1, 0);
+    k_colsum_groups<uint32_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, stride, P.light_buckets, 1, 0, rg);
     k_scan_nodes<<<nn, 1024, 0, st>>>(d_nodes, nn, d_P, d_off, stride, P.light_buckets, 1, 0, d_ntot);
     device_exclusive_scan<uint64_t>(d_ntot, nn, d_nbase, d_part, d_misc + 5, st);
     k_write_X<uint32_t, uint64_t><<<ngrp, 256, 0, st>>>(d_C, d_nodes, d_grp_node, ngrp, d_P, d_X, stride,
-                                                         P.light_buckets, 1, 0, d_nbase);
+                                                         P.light_buckets, 1, 0, d_nbase, rg);
     check_launch();
     tr.launched(6);
 

@@ -60,7 +60,8 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
   constexpr bool kHasV = Cfg::kValBytes > 0;
   constexpr int T = TILE;
   constexpr int ITEMS = T / NT;
-  static_assert(T <= 4096 && ITEMS * NT == T, "tile index is 12 bits");
+  static_assert(T <= 8192 && ITEMS * NT == T, "tile index is 12 or 13 bits");
+  constexpr uint32_t IB = T <= 4096 ? kIdxBits : kIdxBits + 1;   // (bucket << IB) | index
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red64[33];
   __shared__ __align__(8) uint64_t full[STAGES];
@@ -258,7 +259,7 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
       if (b == kSentinel) continue;
       const uint32_t sh = (b & 1u) << 4;
       const uint32_t s = ((mine[b >> 1] >> sh) & 0xFFFFu) + rk[k];
-      srt[s] = (b << kIdxBits) | (w * (32 * ITEMS) + k * 32 + lane);
+      srt[s] = (b << IB) | (w * (32 * ITEMS) + k * 32 + lane);
     }
     csync<NW>();
     mark(4);
@@ -287,7 +288,7 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
           const uint32_t s = threadIdx.x + (k0 + k) * NT;
           ok[k] = s < n_valid;
           const uint32_t ent = ok[k] ? srt[s] : 0u;   // srt beyond n_valid is stale
-          const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
+          const uint32_t b = ent >> IB, i = ent & ((1u << IB) - 1);
           wk[k] = ok[k] && b < key_below;
           dd[k] = rbase + static_cast<uint32_t>(wbase[b] + s);
           kk[k] = rec_key(i);
@@ -310,7 +311,7 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
     } else {
       for (uint32_t s = threadIdx.x; s < n_valid; s += NT) {
         const uint32_t ent = srt[s];
-        const uint32_t b = ent >> kIdxBits, i = ent & ((1u << kIdxBits) - 1);
+        const uint32_t b = ent >> IB, i = ent & ((1u << IB) - 1);
         uint64_t d = rbase + static_cast<uint32_t>(wbase[b] + s);
         if (dbg & 2) d = begin + s;
         if (!(dbg & 1)) {

@@ -131,8 +131,51 @@ k_count(const K* __restrict__ src, const Work* __restrict__ work, uint32_t n_wor
         }
       }
     };
-    if (wids) full_batches(std::true_type{});
-    else full_batches(std::false_type{});
+    // 16-byte key loads and packed id stores when the item is aligned (work
+    // items start at multiples of 8 records: the root's are, deeper nodes'
+    // mostly not); thread t owns records 2048b + V (256 k + t) + [0, V)
+    constexpr uint32_t V = (sizeof(K) == 4 || sizeof(K) == 8) ? 16 / sizeof(K) : 1;
+    const bool vec = V > 1 && kstride == 1 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(wids) & (2 * V - 1)) == 0;
+    auto vec_batches = [&](auto write_ids) {
+      if constexpr (V > 1) {
+        using VT = std::conditional_t<sizeof(K) == 8, ulonglong2, uint4>;
+        using IT = std::conditional_t<V == 2, uint32_t, uint2>;   // V packed u16 ids
+        constexpr uint32_t NV = kCountItems / V;
+        for (uint32_t base = 0; base < full; base += kBatch) {
+          VT kv[NV];
+#pragma unroll
+          for (uint32_t k = 0; k < NV; ++k)
+            kv[k] = __ldg(reinterpret_cast<const VT*>(ws + base) + k * kCountThreads + threadIdx.x);
+#pragma unroll
+          for (uint32_t k = 0; k < NV; ++k) {
+            const K* kk = reinterpret_cast<const K*>(&kv[k]);
+            const uint32_t i0 = base + V * (k * kCountThreads + threadIdx.x);
+            uint32_t bb[V];
+#pragma unroll
+            for (uint32_t v = 0; v < V; ++v) {
+              bb[v] = bf(kk[v], begin + i0 + v, tab);
+              atomicAdd(&cnt[bb[v]], 1u);
+            }
+            if constexpr (decltype(write_ids)::value) {
+              IT packed;
+              uint32_t* pw = reinterpret_cast<uint32_t*>(&packed);
+#pragma unroll
+              for (uint32_t v = 0; v < V; v += 2) pw[v / 2] = bb[v] | (bb[v + 1] << 16);
+              *reinterpret_cast<IT*>(wids + i0) = packed;
+            }
+          }
+        }
+      }
+    };
+    if (vec) {
+      if (wids) vec_batches(std::true_type{});
+      else vec_batches(std::false_type{});
+    } else if (wids) {
+      full_batches(std::true_type{});
+    } else {
+      full_batches(std::false_type{});
+    }
     for (uint32_t base = full; base < len; base += kBatch) {    // tail
       K keys[kCountItems];
 #pragma unroll
@@ -171,13 +214,13 @@ template <typename CT>
 static __global__ void k_colsum_groups(const CT* __restrict__ C, const Node* __restrict__ nodes,
                                 const uint32_t* __restrict__ grp_node, uint32_t n_grps,
                                 uint64_t* __restrict__ P, uint32_t stride, uint32_t n_light,
-                                int light_only, uint32_t fixed_cols) {
+                                int light_only, uint32_t fixed_cols, uint32_t rg = kRowGroup) {
   for (uint32_t g = blockIdx.x; g < n_grps; g += gridDim.x) {
     const Node nd = nodes[grp_node[g]];
     const uint32_t cols = node_cols(nd, n_light, light_only, fixed_cols);
     const uint32_t gi = g - nd.grp_base;
-    const uint64_t r0 = nd.row_base + static_cast<uint64_t>(gi) * kRowGroup;
-    const uint64_t r1 = min(r0 + kRowGroup, nd.row_base + nd.n_rows);
+    const uint64_t r0 = nd.row_base + static_cast<uint64_t>(gi) * rg;
+    const uint64_t r1 = min(r0 + rg, nd.row_base + nd.n_rows);
     for (uint32_t b = threadIdx.x; b < cols; b += blockDim.x) {
       uint64_t s = 0;
       for (uint64_t r = r0; r < r1; ++r) s += C[r * stride + b];
@@ -253,15 +296,15 @@ __global__ void k_write_X(const CT* __restrict__ C, const Node* __restrict__ nod
                           const uint32_t* __restrict__ grp_node, uint32_t n_grps,
                           const uint64_t* __restrict__ P, XT* __restrict__ X, uint32_t stride,
                           uint32_t n_light, int light_only, uint32_t fixed_cols,
-                          const uint64_t* __restrict__ node_base) {
+                          const uint64_t* __restrict__ node_base, uint32_t rg = kRowGroup) {
   for (uint32_t g = blockIdx.x; g < n_grps; g += gridDim.x) {
     const uint32_t j = grp_node[g];
     const Node nd = nodes[j];
     const uint64_t base = node_base ? node_base[j] : nd.out_base;
     const uint32_t cols = node_cols(nd, n_light, light_only, fixed_cols);
     const uint32_t gi = g - nd.grp_base;
-    const uint64_t r0 = nd.row_base + static_cast<uint64_t>(gi) * kRowGroup;
-    const uint64_t r1 = min(r0 + kRowGroup, nd.row_base + nd.n_rows);
+    const uint64_t r0 = nd.row_base + static_cast<uint64_t>(gi) * rg;
+    const uint64_t r1 = min(r0 + rg, nd.row_base + nd.n_rows);
     for (uint32_t b = threadIdx.x; b < cols; b += blockDim.x) {
       uint64_t run = base + P[static_cast<uint64_t>(g) * stride + b];
       for (uint64_t r = r0; r < r1; ++r) {

@@ -168,13 +168,34 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       return;
     }
     const uint32_t b = home(k);
-    TK q[Sh::kW];
+    constexpr uint32_t W = Sh::kW;
+    TK q[W];
     bucket_keys(tk, b, q);
-    uint32_t slot = T;
+    uint32_t slot = T, e = W;
 #pragma unroll
-    for (uint32_t i = 0; i < Sh::kW; ++i)
-      if (q[i] == k) slot = Sh::kW * b + i;
-    if (slot == T) slot = fold_probe<TK, T, Sh::kW>(tk, k, b, q, &s_used, &s_fail, Sh::kLimit);
+    for (int i = W - 1; i >= 0; --i) {
+      if (q[i] == k) slot = W * b + i;
+      if (q[i] == kEmpty) e = i;
+    }
+    if (slot == T) {   // inline the two common misses; the out-of-line probe takes the rest
+      if (e < W) {     // not in the table (slots fill buckets in order): claim the home slot
+        const TK old = atomicCAS(const_cast<TK*>(tk + W * b + e), kEmpty, k);
+        if (old == kEmpty) {
+          slot = W * b + e;
+          if (atomicAdd(&s_used, 1u) >= Sh::kLimit) s_fail = 1;
+        } else if (old == k) {
+          slot = W * b + e;
+        }
+        if (slot == T) slot = fold_probe<TK, T, W>(tk, k, b, q, &s_used, &s_fail, Sh::kLimit);   // lost a race
+      } else {         // home bucket full: the key overflowed into the next one
+        const uint32_t b2 = (b + 1) & (NB - 1);
+        bucket_keys(tk, b2, q);
+#pragma unroll
+        for (uint32_t i = 0; i < W; ++i)
+          if (q[i] == k) slot = W * b2 + i;
+        if (slot == T) slot = fold_probe<TK, T, W>(tk, k, b2, q, &s_used, &s_fail, Sh::kLimit);   // (b2 checked)
+      }
+    }
     if (slot == T) {   // full: only after the limit was passed
       s_fail = 1;
       return;
