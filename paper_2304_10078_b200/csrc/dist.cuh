@@ -187,8 +187,16 @@ struct TileDesc {
   uint32_t node;
   uint64_t row;       // X row of the work item
   uint32_t fresh;     // first tile of its work item
-  uint32_t pad;
+  uint32_t pad;       // staging plan (tile_plan): which streams landed, their element shifts
 };
+
+// Staging plan of a tile, packed by the producer so the consumers do not
+// recompute the Bulk16 supersets: bit 0 ids staged, bit 1 records staged
+// (keys [+ values], or the pair stream), bits 8-11 / 12-15 / 16-19 the
+// element shifts of ids / keys (pairs) / values.
+__device__ __forceinline__ uint32_t tile_plan(bool i_ok, uint32_t i_sh, bool r_ok, uint32_t k_sh, uint32_t v_sh) {
+  return (i_ok ? 1u : 0u) | (r_ok ? 2u : 0u) | (i_sh << 8) | (k_sh << 12) | (v_sh << 16);
+}
 
 // Producer (one thread of the producer warp): claims work items from the
 // global counter *ctr (zeroed by the launcher; items listed longest first),
@@ -248,9 +256,16 @@ __device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __re
     d.node = pw.node;
     d.row = pw.row;
     d.fresh = ptb == 0;
-    d.pad = 0;
-    sdesc[b] = d;
     const Bulk16<uint16_t> bi(ids, n_src, begin, cnt);
+    if constexpr (SA) {
+      const Bulk16<Pair2<K>> bp(reinterpret_cast<const Pair2<K>*>(sk), n_src, begin, cnt);
+      d.pad = tile_plan(bi.ok, bi.sh, bp.ok, bp.sh, 0);
+    } else {
+      const Bulk16<K> bk(sk, n_src, begin, cnt);
+      const Bulk16<V> bv(sv, n_src, begin, cnt);
+      d.pad = tile_plan(bi.ok, bi.sh, bk.ok && (!kHasV || bv.ok), bk.sh, kHasV ? bv.sh : 0);
+    }
+    sdesc[b] = d;
     if constexpr (SA) {   // pair records: one stream into the key + value areas
       const Bulk16<Pair2<K>> bp(reinterpret_cast<const Pair2<K>*>(sk), n_src, begin, cnt);
       fence_proxy_async();

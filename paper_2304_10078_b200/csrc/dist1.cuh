@@ -122,42 +122,57 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
       if constexpr (DA) hbase = n_light < nb ? X[static_cast<uint64_t>(nodes[td.node].row_base) * stride + n_light] : 0;
       for (uint32_t b = threadIdx.x; b < nb; b += NT) cursor[b] = static_cast<uint32_t>(xrow[b] - rbase);
     }
-    const Bulk16<uint16_t> pi(ids, n_src, begin, cnt);
     static_assert(!(SA || DA) || (sizeof(K) == sizeof(V) && ValTraits<V>::bytes == sizeof(K)), "pair layout needs V == K");
+    // staging plan from the producer (tile_plan): staged streams and shifts
+    const uint32_t plan = td.pad;
+    const bool i_ok = plan & 1u;
+    const bool staged = (plan >> 1) & 1u;
+    const uint32_t i_sh = (plan >> 8) & 15u, k_sh = (plan >> 12) & 15u, v_sh = (plan >> 16) & 15u;
     const Pair2<K>* gP = reinterpret_cast<const Pair2<K>*>(sk);
-    const Bulk16<Pair2<K>> pp(gP, n_src, begin, cnt);
-    const Bulk16<K> pk(sk, n_src, begin, cnt);
-    const Bulk16<V> pv(sv, n_src, begin, cnt);
-    const Pair2<K>* tP = reinterpret_cast<const Pair2<K>*>(stK(buf)) + pp.sh;
-    const bool staged = SA ? pp.ok : (pk.ok && (!kHasV || pv.ok));
+    const Pair2<K>* tP = reinterpret_cast<const Pair2<K>*>(stK(buf)) + k_sh;
     auto rec_key = [&](uint32_t i) -> K {   // record i of the tile, staged or from global
       if constexpr (SA) return staged ? tP[i].k : gP[begin + i].k;
-      else return pk.ok ? stK(buf)[pk.sh + i] : sk[begin + i];
+      else return staged ? stK(buf)[k_sh + i] : sk[begin + i];
     };
     auto rec_val = [&](uint32_t i) -> V {
       if constexpr (SA) return static_cast<V>(staged ? tP[i].v : gP[begin + i].v);
-      else return pv.ok ? stV(buf)[pv.sh + i] : sv[begin + i];
+      else return staged ? stV(buf)[v_sh + i] : sv[begin + i];
     };
-    const uint16_t* tI = stI(buf) + pi.sh;
+    const uint16_t* tI = stI(buf) + i_sh;
     mark(0);
 
     // A. in-warp ranks: old value of the warp's packed counter
     uint32_t bk[ITEMS], rk[ITEMS];
+    if (cnt == T && i_ok) {   // full staged tile: no bounds or source checks
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
-      uint32_t b = kSentinel;
-      if (i < cnt) {
-        b = pi.ok ? tI[i] : ids[begin + i];
-        if (b >= nb) b = kSentinel;
+      for (int k = 0; k < ITEMS; ++k) {
+        uint32_t b = tI[w * (32 * ITEMS) + k * 32 + lane];
+        b = b < nb ? b : kSentinel;
+        bk[k] = b;
+        rk[k] = 0;
+        if (b != kSentinel) {
+          const uint32_t sh = (b & 1u) << 4;
+          rk[k] = (atomicAdd(&mine[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
+        }
+        __syncwarp();   // item k's increments precede item k+1's
       }
-      bk[k] = b;
-      rk[k] = 0;
-      if (b != kSentinel) {
-        const uint32_t sh = (b & 1u) << 4;
-        rk[k] = (atomicAdd(&mine[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t i = w * (32 * ITEMS) + k * 32 + lane;
+        uint32_t b = kSentinel;
+        if (i < cnt) {
+          b = i_ok ? tI[i] : ids[begin + i];
+          if (b >= nb) b = kSentinel;
+        }
+        bk[k] = b;
+        rk[k] = 0;
+        if (b != kSentinel) {
+          const uint32_t sh = (b & 1u) << 4;
+          rk[k] = (atomicAdd(&mine[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
+        }
+        __syncwarp();   // item k's increments precede item k+1's
       }
-      __syncwarp();   // item k's increments precede item k+1's
     }
     csync<NW>();
     mark(2);
