@@ -22,10 +22,12 @@
 // written).
 //
 // Table: buckets of 16 bytes (4 u32 or 2 u64 slots), one shared load each;
-// the home bucket is a multiplicative fold of the raw key (independent of
-// the hash bits the node's ancestors bucketed on), slots fill each bucket
-// left to right, the next bucket takes the overflow.  Per record: one
-// vector load, 2-4 compares, one shared atomicAdd (+2 for sums).
+// a key has two candidate buckets -- for u32 keys two multiplicative folds
+// of the raw key (independent of the hash bits the node's ancestors
+// bucketed on), for u64 keys the home fold and the next bucket: the first
+// while it has room, the second when the first is full, the buckets after
+// the second when both are (fold_probe2).  Per record: one or two vector
+// loads, compares, one shared atomicAdd (+1-2 for sums).
 //
 // Output order per node (deterministic whatever the insertion races): by
 // (home bucket, key) -- a counting sort over home buckets, then a key sort
@@ -92,37 +94,50 @@ __device__ __forceinline__ void bucket_keys(const volatile unsigned long long* t
 // since been filled -- filled slots never change -- and the CAS that claims
 // an empty slot returns its current key.)
 
-// Slot of key k: bucket b's keys q were read by the caller and do not hold
-// k.  Claims the first empty slot of the first bucket that has one (slots
-// fill each bucket left to right, overflow goes to the next bucket).
-// Returns T when the table is full.  Out of line: the hot path is the
-// caller's single bucket read.
+// Claims (or finds) the slot of key k when the caller's reads of its two
+// candidate buckets b1, b2 missed.  Placement rule, whatever the races: b1's
+// first empty slot; b2 only when b1 is full; past b2 (next buckets in
+// order) only when both are full -- buckets never lose keys, so a lookup
+// that finds an empty slot in b1 (or, with b1 full, in b2) knows k is
+// absent.  Every CAS result is checked, so a slot another thread filled
+// with k is found.  Returns T when the table is full.  Out of line: only
+// inserts that lost a race and keys past both buckets come here.
 template <typename TK, uint32_t T, uint32_t W>
-__device__ __noinline__ uint32_t fold_probe(volatile TK* tk, TK k, uint32_t b, const TK* q0, uint32_t* used,
-                                            uint32_t* fail, uint32_t limit) {
+__device__ __noinline__ uint32_t fold_probe2(volatile TK* tk, TK k, uint32_t b1, uint32_t b2, uint32_t* used,
+                                             uint32_t* fail, uint32_t limit) {
   constexpr uint32_t NB = T / W;
   constexpr TK kEmpty = ~TK(0);
-  TK q[W];
-#pragma unroll
-  for (uint32_t i = 0; i < W; ++i) q[i] = q0[i];
-  for (uint32_t step = 0; step < NB; ++step) {
+  auto in_bucket = [&](uint32_t b, uint32_t& slot) -> bool {   // true: k found or placed in b
+    TK q[W];
+    bucket_keys(tk, b, q);
     uint32_t e = W;
 #pragma unroll
-    for (int i = W - 1; i >= 0; --i)
+    for (int i = W - 1; i >= 0; --i) {
+      if (q[i] == k) {
+        slot = W * b + i;
+        return true;
+      }
       if (q[i] == kEmpty) e = i;
+    }
     for (; e < W; ++e) {
       const TK old = atomicCAS(const_cast<TK*>(tk + W * b + e), kEmpty, k);
       if (old == kEmpty) {
         if (atomicAdd(used, 1u) >= limit) *fail = 1;
-        return W * b + e;
+        slot = W * b + e;
+        return true;
       }
-      if (old == k) return W * b + e;
+      if (old == k) {
+        slot = W * b + e;
+        return true;
+      }
     }
+    return false;   // b is full and does not hold k
+  };
+  uint32_t slot = T;
+  if (in_bucket(b1, slot) || in_bucket(b2, slot)) return slot;
+  for (uint32_t step = 1, b = b2; step < NB; ++step) {
     b = (b + 1) & (NB - 1);
-    bucket_keys(tk, b, q);
-#pragma unroll
-    for (uint32_t i = 0; i < W; ++i)
-      if (q[i] == k) return W * b + i;
+    if (b != b1 && in_bucket(b, slot)) return slot;
   }
   return T;
 }
@@ -153,6 +168,10 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
   const volatile uint32_t* vfail = &s_fail;
 
   auto home = [](TK k) { return static_cast<uint32_t>((static_cast<uint64_t>(k) * kGamma) >> (64 - Sh::kLog2B)); };
+  auto home2 = [](TK k, uint32_t b1) {   // a second fold, never b1
+    const uint32_t b = static_cast<uint32_t>((static_cast<uint64_t>(k) * kMul2) >> (64 - Sh::kLog2B));
+    return b == b1 ? b ^ 1u : b;
+  };
   auto add_sum = [&](uint32_t* lo, uint32_t* hi, uint64_t v) {
     const uint32_t l = static_cast<uint32_t>(v), h = static_cast<uint32_t>(v >> 32);
     const uint32_t old = atomicAdd(lo, l);
@@ -167,34 +186,51 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       if constexpr (SUM) add_sum(&e_lo, &e_hi, v);
       return;
     }
-    const uint32_t b = home(k);
+    // u32 keys (many per node: c4 ~9.8K at load 0.6): two candidate buckets
+    // (multiplicative folds of the raw key), both read every time -- no
+    // data-dependent probe loop, so warps do not diverge on overflow keys.
+    // u64 keys: the home bucket, then the next one only when it is full
+    // (their nodes hold few keys; a second load per record cost more than
+    // the rare overflow)
     constexpr uint32_t W = Sh::kW;
-    TK q[W];
-    bucket_keys(tk, b, q);
-    uint32_t slot = T, e = W;
+    constexpr bool kTwo = sizeof(K) == 4;
+    const uint32_t b1 = home(k), b2 = kTwo ? home2(k, b1) : (b1 + 1) & (NB - 1);
+    TK q1[W], q2[W];
+    bucket_keys(tk, b1, q1);
+    uint32_t slot = T, e1 = W, e2 = W;
+    if constexpr (kTwo) bucket_keys(tk, b2, q2);
 #pragma unroll
     for (int i = W - 1; i >= 0; --i) {
-      if (q[i] == k) slot = W * b + i;
-      if (q[i] == kEmpty) e = i;
+      if (q1[i] == k) slot = W * b1 + i;
+      if (q1[i] == kEmpty) e1 = i;
+      if constexpr (kTwo) {
+        if (q2[i] == k) slot = W * b2 + i;
+        if (q2[i] == kEmpty) e2 = i;
+      }
     }
-    if (slot == T) {   // inline the two common misses; the out-of-line probe takes the rest
-      if (e < W) {     // not in the table (slots fill buckets in order): claim the home slot
-        const TK old = atomicCAS(const_cast<TK*>(tk + W * b + e), kEmpty, k);
+    if constexpr (!kTwo) {
+      if (slot == T && e1 == W) {   // home bucket full: read the next one
+        bucket_keys(tk, b2, q2);
+#pragma unroll
+        for (int i = W - 1; i >= 0; --i) {
+          if (q2[i] == k) slot = W * b2 + i;
+          if (q2[i] == kEmpty) e2 = i;
+        }
+      }
+    }
+    if (slot == T) {   // absent (or beyond both buckets): one inline claim attempt
+      const bool at1 = e1 < W;
+      if (at1 || e2 < W) {
+        const uint32_t cs = at1 ? W * b1 + e1 : W * b2 + e2;
+        const TK old = atomicCAS(const_cast<TK*>(tk + cs), kEmpty, k);
         if (old == kEmpty) {
-          slot = W * b + e;
+          slot = cs;
           if (atomicAdd(&s_used, 1u) >= Sh::kLimit) s_fail = 1;
         } else if (old == k) {
-          slot = W * b + e;
+          slot = cs;
         }
-        if (slot == T) slot = fold_probe<TK, T, W>(tk, k, b, q, &s_used, &s_fail, Sh::kLimit);   // lost a race
-      } else {         // home bucket full: the key overflowed into the next one
-        const uint32_t b2 = (b + 1) & (NB - 1);
-        bucket_keys(tk, b2, q);
-#pragma unroll
-        for (uint32_t i = 0; i < W; ++i)
-          if (q[i] == k) slot = W * b2 + i;
-        if (slot == T) slot = fold_probe<TK, T, W>(tk, k, b2, q, &s_used, &s_fail, Sh::kLimit);   // (b2 checked)
       }
+      if (slot == T) slot = fold_probe2<TK, T, W>(tk, k, b1, b2, &s_used, &s_fail, Sh::kLimit);
     }
     if (slot == T) {   // full: only after the limit was passed
       s_fail = 1;
