@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(NT + 32, 1)   // 17 warps: one sub-partition h
 k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
               K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
               const Node* __restrict__ nodes, const uint64_t* __restrict__ X, uint32_t stride, uint32_t keep_below,
-              uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr, uint32_t key_below) {
+              uint32_t n_light, uint32_t fixed_nb, uint32_t* __restrict__ ctr, uint32_t key_below,
+              uint32_t cstride) {   // cstride: shared counter / cursor rows (>= every work item's nb)
   using Cfg = Dist1Cfg<K, V, TILE, NT, STAGES>;
   constexpr int NW = NT / 32;
   constexpr bool kHasV = Cfg::kValBytes > 0;
@@ -71,11 +72,11 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
   auto stI = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * Cfg::kSet); };
   auto stK = [&](int b) { return reinterpret_cast<K*>(smem + b * Cfg::kSet + Cfg::kBufI); };
   auto stV = [&](int b) { return reinterpret_cast<V*>(smem + b * Cfg::kSet + Cfg::kBufI + Cfg::kBufK); };
-  const uint32_t pstride = Cfg::pair_stride(stride);
+  const uint32_t pstride = Cfg::pair_stride(cstride);
   unsigned char* p = smem + STAGES * Cfg::kSet;
   uint32_t* srt = reinterpret_cast<uint32_t*>(p); p += T * 4;
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
-  uint32_t* wbase = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(stride) * 4);
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(cstride) * 4);
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(p); p += Cfg::up16(static_cast<size_t>(cstride) * 4);
   uint32_t* cntw = reinterpret_cast<uint32_t*>(p);   // [NW][pstride] u16 pairs
   for (uint32_t i = threadIdx.x; i < NW * pstride; i += blockDim.x) cntw[i] = 0;
   const int dbg = g_dist_debug;

@@ -54,18 +54,18 @@ inline void launch_distribute_t(const K* sk, const V* sv, const uint16_t* ids, u
   check_launch();
 }
 
-template <typename K, typename V, int TILE, bool SA, bool DA>
+template <typename K, typename V, int TILE, bool SA, bool DA, int STAGES = 2>
 inline void launch_distribute1_t(const K* sk, const V* sv, const uint16_t* ids, uint64_t n_src, K* dk, V* dv,
                                  const Work* d_work, uint32_t nwork, const Node* d_nodes, const uint64_t* d_X,
                                  uint32_t stride, uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb,
-                                 cudaStream_t st, uint32_t* ctr, uint32_t key_below) {
-  const size_t dsm = Dist1Cfg<K, V, TILE, 512, 2>::smem_bytes(stride);
-  auto kern = k_distribute1<K, V, TILE, 512, 2, SA, DA>;
+                                 cudaStream_t st, uint32_t* ctr, uint32_t key_below, uint32_t cstride) {
+  const size_t dsm = Dist1Cfg<K, V, TILE, 512, STAGES>::smem_bytes(cstride);
+  auto kern = k_distribute1<K, V, TILE, 512, STAGES, SA, DA>;
   SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
   const uint32_t grid = std::min<uint32_t>(nwork, 148u);
   SS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
   kern<<<grid, 512 + 32, dsm, st>>>(sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below,
-                                    n_light, fixed_nb, ctr, key_below);
+                                    n_light, fixed_nb, ctr, key_below, cstride);
   check_launch();
 }
 
@@ -78,7 +78,8 @@ inline bool dist_radix_forced() {
 // 8192-record tiles when a staged record is <= 8 bytes (measured: c4's u32
 // distribute 7.1 -> 5.3 ms).  For 16-byte records the stage would not fit;
 // an ids-only stage with the records prefetched into L2 and gathered by the
-// write-out was measured slower than 4096 staged (c2 13.3 -> 15.6 ms).
+// write-out was measured slower than 4096 staged (c2 13.3 -> 15.6 ms), and
+// so were three stages of 3072 (12.8 -> 14.1 ms; c3 10.1 -> 11.0 ms).
 template <typename K, typename V>
 constexpr bool kDist8k = sizeof(K) + ValTraits<V>::bytes <= 8;
 
@@ -105,8 +106,15 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
                               uint32_t nwork, const Node* d_nodes, const uint64_t* d_X, uint32_t stride,
                               uint32_t keep_below, uint32_t n_light, uint32_t fixed_nb, cudaStream_t st,
                               uint64_t n_src, uint32_t* ctr, uint32_t key_below = 0xFFFFFFFFu,
-                              bool src_pairs = false, bool dst_pairs = false) {
+                              bool src_pairs = false, bool dst_pairs = false, uint32_t max_nb = 0) {
   if (!nwork) return;
+  // shared counter rows: the largest bucket count a work item can have
+  // (max_nb: n_light + the level's largest n_heavy, when the caller knows it)
+  uint32_t cstride = stride;
+  if (fixed_nb && fixed_nb < cstride) cstride = fixed_nb;
+  if (keep_below < cstride) cstride = keep_below;
+  if (max_nb && max_nb < cstride) cstride = max_nb;
+  cstride = std::max<uint32_t>(2, std::min<uint32_t>(stride, (cstride + 1) & ~1u));
   static const int dbg = [] {
     const char* e = std::getenv("SS_DIST_DEBUG");
     const int v = e ? std::atoi(e) : 0;
@@ -117,15 +125,16 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
   if (stride >= kMaxDistBuckets) throw Fail(SS_ERR_CONFIG, "too many buckets for the GPU distribute");
 #define SS_DIST_ARGS \
   sk, sv, ids, n_src, dk, dv, d_work, nwork, d_nodes, d_X, stride, keep_below, n_light, fixed_nb, st, ctr
-  const int t1 = dist1_tile<K, V>(stride, n_src);
+  const int t1 = dist1_tile<K, V>(cstride, n_src);
   if (t1) {
     auto go = [&]<int TILE>() {
       if constexpr (std::is_same_v<K, V>) {
-        if (src_pairs && dst_pairs) return launch_distribute1_t<K, V, TILE, true, true>(SS_DIST_ARGS, key_below);
-        if (src_pairs) return launch_distribute1_t<K, V, TILE, true, false>(SS_DIST_ARGS, key_below);
-        if (dst_pairs) return launch_distribute1_t<K, V, TILE, false, true>(SS_DIST_ARGS, key_below);
+        if (src_pairs && dst_pairs)
+          return launch_distribute1_t<K, V, TILE, true, true>(SS_DIST_ARGS, key_below, cstride);
+        if (src_pairs) return launch_distribute1_t<K, V, TILE, true, false>(SS_DIST_ARGS, key_below, cstride);
+        if (dst_pairs) return launch_distribute1_t<K, V, TILE, false, true>(SS_DIST_ARGS, key_below, cstride);
       }
-      launch_distribute1_t<K, V, TILE, false, false>(SS_DIST_ARGS, key_below);
+      launch_distribute1_t<K, V, TILE, false, false>(SS_DIST_ARGS, key_below, cstride);
     };
     if constexpr (kDist8k<K, V>) {
       if (t1 == 8192) return go.template operator()<8192>();
