@@ -349,6 +349,69 @@ k_leaf_eq_global(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, 
   }
 }
 
+// Mid-size leaves (kLeafSmemMax, alpha): up to kLeafMidMax<K, V> records
+// stage records and work arrays in shared memory (one CTA per SM); larger
+// ones keep k_leaf_eq_global's global-scratch path.  The global path costs
+// ~10x per record (its probes and counters are L2 round trips): c2's 2053
+// mid leaves took 0.42 ms there.
+template <typename K, typename V>
+constexpr uint32_t kLeafMidMax = sizeof(K) + ValTraits<V>::bytes <= 16 ? 4096u : 2048u;
+
+template <typename K, typename V>
+__host__ inline size_t leaf_mid_smem_bytes() {
+  constexpr uint32_t M = kLeafMidMax<K, V>;
+  return static_cast<size_t>(M) * (sizeof(K) + ValTraits<V>::bytes) + leaf_words(M, false) * 4 + 64;
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(kLeafThreads)
+k_leaf_eq_mid(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* __restrict__ A_v,
+              const Leaf* __restrict__ leaves, uint32_t n_leaves, int in_a, int identity,
+              uint32_t* __restrict__ scratch, uint64_t words_per_cta, int hw, int s_pairs = 0) {
+  constexpr bool kHasV = ValTraits<V>::bytes > 0;
+  constexpr uint32_t M = kLeafMidMax<K, V>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t red[33];
+  K* rk = reinterpret_cast<K*>(smem);
+  V* rv = reinterpret_cast<V*>(rk + M);
+  uint32_t* work = reinterpret_cast<uint32_t*>(kHasV ? reinterpret_cast<unsigned char*>(rv + M)
+                                                     : reinterpret_cast<unsigned char*>(rv));
+  uint32_t* mine = scratch + static_cast<uint64_t>(blockIdx.x) * words_per_cta;
+  // where the leaf lives: A, or S (pair records when s_pairs)
+  const K* src_k = in_a ? A_k : S_k;
+  const V* src_v = in_a ? A_v : S_v;
+  const uint32_t ss = in_a ? 1u : (s_pairs ? 2u : 1u);
+  for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
+    const Leaf lf = leaves[l];
+    const uint32_t m = static_cast<uint32_t>(lf.size);
+    if (m <= M) {
+      if (m <= 1) {
+        if (m == 1 && threadIdx.x == 0 && !in_a) {
+          A_k[lf.lo] = src_k[lf.lo * ss];
+          if constexpr (kHasV) A_v[lf.lo] = src_v[lf.lo * ss];
+        }
+        __syncthreads();
+        continue;
+      }
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        rk[i] = src_k[(lf.lo + i) * ss];
+        if constexpr (kHasV) rv[i] = src_v[(lf.lo + i) * ss];
+      }
+      __syncthreads();
+      LeafArrays a = leaf_arrays(work, leaf_cap(m), m, false);
+      leaf_eq(rk, rv, A_k + lf.lo, A_v + lf.lo, m, identity != 0, a, red, hw != 0);
+      __syncthreads();
+      continue;
+    }
+    K* sk;
+    V* sv;
+    leaf_stage(S_k, S_v, A_k, A_v, lf, in_a, s_pairs, sk, sv);
+    LeafArrays a = leaf_arrays(mine, leaf_cap(m), m, false);
+    leaf_eq(sk, sv, A_k + lf.lo, A_v + lf.lo, m, identity != 0, a, red, hw != 0);
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // semisort< base case: stable sort by key (core.py:425-429)
 // ---------------------------------------------------------------------------

@@ -360,6 +360,12 @@ struct SortEngine {
     if (mode == SS_MODE_LT) {
       k_leaf_lt<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count),
                                                     in_a, scr, words, aos ? 1 : 0);
+    } else if (grid > 1) {   // planned mid leaves: shared-memory path up to kLeafMidMax
+      const size_t sm = leaf_mid_smem_bytes<K, V>();
+      auto kern = k_leaf_eq_mid<K, V>;
+      SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      kern<<<grid, kLeafThreads, sm, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count), in_a, identity,
+                                           scr, words, hw_rank_ok() ? 1 : 0, aos ? 1 : 0);
     } else {
       k_leaf_eq_global<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list,
                                                             static_cast<uint32_t>(count), in_a, identity, scr, words,
