@@ -64,7 +64,42 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restric
     const uint64_t begin = wk.begin;
     const uint32_t len = wk.len;
     const uint32_t nl = bf.n_light;
-    for (uint32_t base = 0; base < len; base += kCountThreads * kCountItems) {
+    uint32_t done = 0;
+    if constexpr (!SUM && (sizeof(K) == 4 || sizeof(K) == 8)) {
+      // counting: 16-byte key loads and packed id stores over the aligned
+      // full batches (work items start at multiples of 8 records)
+      constexpr uint32_t V = 16 / sizeof(K), NV = kCountItems / V, kBatch = kCountThreads * kCountItems;
+      using VT = std::conditional_t<sizeof(K) == 8, ulonglong2, uint4>;
+      using IT = std::conditional_t<V == 2, uint32_t, uint2>;
+      const K* ws = src + begin;
+      uint16_t* wids = ids_out + begin;
+      if (ss == 1 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 && (reinterpret_cast<uintptr_t>(wids) & (2 * V - 1)) == 0) {
+        done = len - len % kBatch;
+        for (uint32_t base = 0; base < done; base += kBatch) {
+          VT kv[NV];
+#pragma unroll
+          for (uint32_t k = 0; k < NV; ++k)
+            kv[k] = __ldg(reinterpret_cast<const VT*>(ws + base) + k * kCountThreads + threadIdx.x);
+#pragma unroll
+          for (uint32_t k = 0; k < NV; ++k) {
+            const K* kk = reinterpret_cast<const K*>(&kv[k]);
+            const uint32_t i0 = base + V * (k * kCountThreads + threadIdx.x);
+            uint32_t bb[V];
+#pragma unroll
+            for (uint32_t v = 0; v < V; ++v) {
+              bb[v] = bf(kk[v], begin + i0 + v);
+              atomicAdd(&cnt[bb[v]], 1u);
+            }
+            IT packed;
+            uint32_t* pw = reinterpret_cast<uint32_t*>(&packed);
+#pragma unroll
+            for (uint32_t v = 0; v < V; v += 2) pw[v / 2] = bb[v] | (bb[v + 1] << 16);
+            *reinterpret_cast<IT*>(wids + i0) = packed;
+          }
+        }
+      }
+    }
+    for (uint32_t base = done; base < len; base += kCountThreads * kCountItems) {
       K keys[kCountItems];
       uint64_t vals[SUM ? kCountItems : 1];
 #pragma unroll
