@@ -540,6 +540,10 @@ struct AggEngine {
     const K* sk = B_k[lvl & 1];
     const V* sv = B_v[lvl & 1];
     std::vector<Node> rest, fold;
+    // the table's shared memory (+ ~12 KB static) must fit a CTA: large
+    // light_buckets settings keep the level path
+    const size_t sm = node_fold_smem(sizeof(K), sum(), P.light_buckets);
+    if (sm + 12 * 1024 > 227 * 1024) return cur;
     for (const Node& nd : cur) (nd.size >> 32 ? rest : fold).push_back(nd);
     if (fold.empty()) return rest;
     const uint32_t nn = static_cast<uint32_t>(fold.size());
@@ -569,7 +573,6 @@ struct AggEngine {
     bf.light_bits = P.light_bits;
     bf.identity = identity;
     tr.begin(kPhLeaves);
-    const size_t sm = node_fold_smem(sizeof(K), sum(), P.light_buckets);
     auto launch = [&](auto kern) {
       SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
       int dev = 0, sms = 148;

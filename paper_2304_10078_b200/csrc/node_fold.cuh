@@ -60,17 +60,21 @@ template <> struct FoldKey<uint64_t> {
 // Table geometry: key + record count (+ sum as low and high words -- 32-bit
 // shared atomics, carries out of the low word go to the high word; a 64-bit
 // shared atomicAdd is a CAS spin loop on sm_100) + one counter per bucket
-// for the emission sort.
+// for the emission sort.  u32 counting (c4: ~9.8K keys per node) packs the
+// record counts and the bucket counters as 16-bit halves: 32K slots fit
+// (load 0.3, overflow past both candidate buckets is rare); a count that
+// wraps is caught by the node total (the node then takes the level path).
 template <typename K, bool SUM>
 struct FoldShape {
-  static constexpr uint32_t kLog2T = (sizeof(K) == 4 && !SUM) ? 14u : 13u;
+  static constexpr bool kC16 = sizeof(K) == 4 && !SUM;
+  static constexpr uint32_t kLog2T = kC16 ? 15u : 13u;
   static constexpr uint32_t kT = 1u << kLog2T;
   static constexpr uint32_t kW = 16 / sizeof(K);   // slots per bucket: one 16-byte shared load
   static constexpr uint32_t kLog2B = kLog2T - (sizeof(K) == 4 ? 2u : 1u);
   static constexpr uint32_t kB = kT / kW;
   static constexpr uint32_t kLimit = kT / 4 * 3;   // distinct keys (load 0.75)
   static constexpr uint32_t kPer = kT / kFoldThreads;
-  static constexpr size_t kBytes = static_cast<size_t>(kT) * (sizeof(K) + (SUM ? 12 : 4)) + kB * 4;
+  static constexpr size_t kBytes = static_cast<size_t>(kT) * (sizeof(K) + (kC16 ? 2 : SUM ? 12 : 4)) + kB * (kC16 ? 2 : 4);
 };
 
 __host__ inline size_t node_fold_smem(int key_bytes, bool sum, uint32_t n_light) {
@@ -155,11 +159,29 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
   constexpr TK kEmpty = FK::kEmpty;
   extern __shared__ __align__(16) unsigned char smem[];
   volatile TK* tk = reinterpret_cast<volatile TK*>(smem);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + T * sizeof(TK));
+  constexpr bool C16 = Sh::kC16;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + T * sizeof(TK));   // C16: two 16-bit counts per word
   uint32_t* slo = cnt + T;   // SUM only
   uint32_t* shi = slo + T;
-  uint32_t* hcnt = SUM ? shi + T : cnt + T;   // keys per home bucket, then their scan
-  uint32_t* lcnt = hcnt + NB;
+  uint32_t* hcnt = SUM ? shi + T : cnt + (C16 ? T / 2 : T);   // per home bucket: keys, bases, cursors
+  uint32_t* lcnt = hcnt + (C16 ? NB / 2 : NB);
+  // 16-bit-or-32-bit counter access
+  auto c_add = [&](uint32_t* a, uint32_t i) {   // returns the old value
+    if constexpr (C16) {
+      const uint32_t sh = (i & 1u) << 4;
+      return (atomicAdd(&a[i >> 1], 1u << sh) >> sh) & 0xFFFFu;
+    } else {
+      return atomicAdd(&a[i], 1u);
+    }
+  };
+  auto c_red = [&](uint32_t* a, uint32_t i) {   // no return value
+    if constexpr (C16) atomicAdd(&a[i >> 1], 1u << ((i & 1u) << 4));
+    else atomicAdd(&a[i], 1u);
+  };
+  auto c_get = [&](const uint32_t* a, uint32_t i) -> uint32_t {
+    if constexpr (C16) return (a[i >> 1] >> ((i & 1u) << 4)) & 0xFFFFu;
+    else return a[i];
+  };
   __shared__ HeavySmem tab;
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_node, s_used, s_fail, s_kids, s_max, s_light;
@@ -236,7 +258,7 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       s_fail = 1;
       return;
     }
-    atomicAdd(&cnt[slot], 1u);
+    c_red(cnt, slot);
     if constexpr (SUM) add_sum(&slo[slot], &shi[slot], v);
   };
 
@@ -256,10 +278,10 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
     bf.prepare(nd, j, &tab);
     for (uint32_t s = threadIdx.x; s < T; s += kFoldThreads) {
       tk[s] = kEmpty;
-      cnt[s] = 0;
       if constexpr (SUM) slo[s] = shi[s] = 0;
     }
-    for (uint32_t b = threadIdx.x; b < NB; b += kFoldThreads) hcnt[b] = 0;
+    for (uint32_t s = threadIdx.x; s < (C16 ? T / 2 : T); s += kFoldThreads) cnt[s] = 0;
+    for (uint32_t b = threadIdx.x; b < (C16 ? NB / 2 : NB); b += kFoldThreads) hcnt[b] = 0;
     for (uint32_t b = threadIdx.x; b < bf.n_light; b += kFoldThreads) lcnt[b] = 0;
     __syncthreads();
 
@@ -348,18 +370,23 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       continue;
     }
 
-    // ---- per distinct key: light child (bucket, records), home-group rank -
-    uint32_t gidx[Sh::kPer];
-#pragma unroll
+    // ---- per distinct key: light child (bucket, records), home-group size
+    uint32_t counted = 0;   // C16: all records seen through the 16-bit counts
+#pragma unroll 4
     for (uint32_t r = 0; r < Sh::kPer; ++r) {
       const uint32_t s = r * kFoldThreads + threadIdx.x;
       const TK k = tk[s];
       if (k == kEmpty) continue;
-      gidx[r] = atomicAdd(&hcnt[home(k)], 1u);
+      c_red(hcnt, home(k));
+      const uint32_t c = c_get(cnt, s);
+      counted += c;
       const K key = static_cast<K>(k);
       const uint64_t h = key_hash(key, identity);
       if (bf.n_heavy && heavy_find(tab, KeyTraits<K>::widen(key), h, identity) >= 0) continue;
-      atomicAdd(&lcnt[bf.lc.id(h)], cnt[s]);
+      atomicAdd(&lcnt[bf.lc.id(h)], c);
+    }
+    if constexpr (C16) {   // a wrapped 16-bit count loses records: the node takes the level path
+      if (counted) atomicAdd(&s_used, counted);   // (s_used is free after the stream)
     }
     if (threadIdx.x == 0 && e_cnt) {
       const K key = static_cast<K>(kEmpty);
@@ -387,12 +414,14 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
     uint32_t hc[kBP], run = 0;
 #pragma unroll
     for (uint32_t r = 0; r < kBP; ++r) {
-      hc[r] = hcnt[threadIdx.x * kBP + r];
+      hc[r] = c_get(hcnt, threadIdx.x * kBP + r);
       run += hc[r];
     }
     uint32_t total;
     uint32_t before = block_excl_scan<uint32_t>(run, red, total);   // (its barriers order the atomics above)
-    if (s_max >= alpha) {   // a child would recurse (aggregate.py:139-141): the level path takes the node
+    bool wrapped = false;   // s_used = inserts (= total) + all records counted
+    if constexpr (C16) wrapped = s_used - total != static_cast<uint32_t>(m) - e_cnt;
+    if (s_max >= alpha || wrapped) {   // a child would recurse (aggregate.py:139-141): the level path takes the node
       if (threadIdx.x == 0) {
         G[j] = 0;
         stat[2 * j] = 0;
@@ -401,10 +430,18 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       __syncthreads();
       continue;
     }
+    if constexpr (C16) {   // this thread's kBP (even) buckets are whole words
 #pragma unroll
-    for (uint32_t r = 0; r < kBP; ++r) {
-      hcnt[threadIdx.x * kBP + r] = before;
-      before += hc[r];
+      for (uint32_t r = 0; r < kBP; r += 2) {
+        hcnt[(threadIdx.x * kBP + r) >> 1] = before | ((before + hc[r]) << 16);
+        before += hc[r] + hc[r + 1];
+      }
+    } else {
+#pragma unroll
+      for (uint32_t r = 0; r < kBP; ++r) {
+        hcnt[threadIdx.x * kBP + r] = before;
+        before += hc[r];
+      }
     }
     __syncthreads();
 
@@ -412,15 +449,17 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
     const uint32_t g0 = e_cnt ? 1u : 0u;
     K* ok = st_k + lo + g0;
     uint64_t* oa = st_a + lo + g0;
-#pragma unroll
+    // cursor per home bucket (its base, advanced here): arbitrary order inside
+    // a group, fixed by the key sort below
+#pragma unroll 4
     for (uint32_t r = 0; r < Sh::kPer; ++r) {
       const uint32_t s = r * kFoldThreads + threadIdx.x;
       const TK k = tk[s];
       if (k == kEmpty) continue;
-      const uint32_t at = hcnt[home(k)] + gidx[r];
+      const uint32_t at = c_add(hcnt, home(k));
       ok[at] = static_cast<K>(k);
       if constexpr (SUM) oa[at] = (static_cast<uint64_t>(shi[s]) << 32) | slo[s];
-      else oa[at] = cnt[s];
+      else oa[at] = c_get(cnt, s);
     }
     if (threadIdx.x == 0) {
       if (g0) {
@@ -432,9 +471,10 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       stat[2 * j + 1] = s_kids;
     }
     __syncthreads();   // the staged pairs are visible to the whole CTA
-    // key order inside each home group (groups are small: ~load x 4 keys)
+    // key order inside each home group (groups are small: ~load x 4 keys);
+    // the cursors now hold each group's end
     for (uint32_t b = threadIdx.x; b < NB; b += kFoldThreads) {
-      const uint32_t a = hcnt[b], e = b + 1 < NB ? hcnt[b + 1] : total;
+      const uint32_t a = b ? c_get(hcnt, b - 1) : 0u, e = c_get(hcnt, b);
       for (uint32_t x = a + 1; x < e; ++x) {
         const K kx = ok[x];
         const uint64_t vx = oa[x];

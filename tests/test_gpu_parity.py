@@ -328,6 +328,10 @@ def _fold_cases():
     k64[rng.integers(0, n, 3000)] = u64max
     wide = rng.integers(0, 2**63, 1 << 22).astype(np.uint64)   # level-2 nodes overflow the table
     few = rng.integers(0, 1000, n).astype(np.uint64)            # children >= alpha: nodes recurse
+    # one key with > 65535 records inside an eligible level-2 node: its
+    # 16-bit fold count wraps, the node total catches it (level path)
+    wrap = rng.integers(0, 2000, 1 << 21).astype(np.uint32)
+    wrap[rng.choice(1 << 21, 70000, replace=False)] = np.uint32(12345)
     vals = lambda m: rng.integers(0, 2**64 - 1, m, dtype=np.uint64, endpoint=True)  # noqa: E731
     return [
         ("u32_marker", k32, vals(n), {"light_buckets": 64, "base_case_cutoff": 4096}, False),
@@ -336,6 +340,7 @@ def _fold_cases():
         ("identity", k32.astype(np.uint64), vals(n), {"light_buckets": 32, "base_case_cutoff": 4096}, True),
         ("wide_overflow", wide, vals(len(wide)), {"light_buckets": 64, "base_case_cutoff": 16384}, False),
         ("few_recurse", few, vals(n), {"light_buckets": 4, "base_case_cutoff": 16384}, False),
+        ("u16_wrap", wrap, vals(len(wrap)), {"light_buckets": 16, "base_case_cutoff": 1 << 17, "max_heavy": 0}, False),
     ]
 
 
@@ -348,6 +353,7 @@ def test_node_fold_vs_oracle_and_level_path(S, case, monkeypatch):
     P = S.TuningParams.for_input(n, **kw)
     OP = O.OracleParams.derive(n, **kw)
     adp = S.UIntKeyAdapter(identity=ident)
+    folded = {}
     for kind, spec in (("count", S.ReduceSpec.counting()), ("sum64", S.ReduceSpec.summing64())):
         runs = {}
         for mode in ("1", "0"):
@@ -365,6 +371,7 @@ def test_node_fold_vs_oracle_and_level_path(S, case, monkeypatch):
             assert {int(k): v for k, v in tel.matrix_cells_by_level.items()} == \
                 {int(k): v for k, v in otel.matrix_cells_by_level.items()}
         assert runs["0"][1].nodes_folded == 0
+        folded[kind] = runs["1"][1].nodes_folded
         if name == "wide_overflow":
             assert runs["1"][1].nodes_folded == 0, name   # every level-2 node overflowed
         elif name != "few_recurse":   # (its level-2 nodes recurse; deeper ones may fold)
@@ -374,3 +381,5 @@ def test_node_fold_vs_oracle_and_level_path(S, case, monkeypatch):
         k1, a1 = S.collect_reduce(S.RecordArray(keys, vals), adp, spec, P).to_numpy()
         k2, a2 = res2.to_numpy()
         assert np.array_equal(k1, k2) and np.array_equal(a1, a2)
+    if name == "u16_wrap":   # the hot key's node folds with 32-bit sum-side counts, not with 16-bit ones
+        assert folded["count"] == folded["sum64"] - 1, folded
