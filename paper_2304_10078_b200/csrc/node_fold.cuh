@@ -22,12 +22,13 @@
 // written).
 //
 // Table: buckets of 16 bytes (4 u32 or 2 u64 slots), one shared load each;
-// a key has two candidate buckets -- for u32 keys two multiplicative folds
-// of the raw key (independent of the hash bits the node's ancestors
-// bucketed on), for u64 keys the home fold and the next bucket: the first
-// while it has room, the second when the first is full, the buckets after
-// the second when both are (fold_probe2).  Per record: one or two vector
-// loads, compares, one shared atomicAdd (+1-2 for sums).
+// a key's home bucket is a multiplicative fold of the raw key (independent
+// of the hash bits the node's ancestors bucketed on); slots fill a bucket
+// left to right, the next bucket takes the overflow, the ones after it
+// when both are full (fold_probe2).  Per record: one vector load (two when
+// the home bucket is full), compares, one shared atomicAdd (+1-2 for sums).
+// The kernel is bound by shared-memory wavefronts (bank conflicts of the
+// random bucket loads and counter atomics), not by HBM.
 //
 // Output order per node (deterministic whatever the insertion races): by
 // (home bucket, key) -- a counting sort over home buckets, then a key sort
@@ -190,10 +191,6 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
   const volatile uint32_t* vfail = &s_fail;
 
   auto home = [](TK k) { return static_cast<uint32_t>((static_cast<uint64_t>(k) * kGamma) >> (64 - Sh::kLog2B)); };
-  auto home2 = [](TK k, uint32_t b1) {   // a second fold, never b1
-    const uint32_t b = static_cast<uint32_t>((static_cast<uint64_t>(k) * kMul2) >> (64 - Sh::kLog2B));
-    return b == b1 ? b ^ 1u : b;
-  };
   auto add_sum = [&](uint32_t* lo, uint32_t* hi, uint64_t v) {
     const uint32_t l = static_cast<uint32_t>(v), h = static_cast<uint32_t>(v >> 32);
     const uint32_t old = atomicAdd(lo, l);
@@ -208,36 +205,26 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
       if constexpr (SUM) add_sum(&e_lo, &e_hi, v);
       return;
     }
-    // u32 keys (many per node: c4 ~9.8K at load 0.6): two candidate buckets
-    // (multiplicative folds of the raw key), both read every time -- no
-    // data-dependent probe loop, so warps do not diverge on overflow keys.
-    // u64 keys: the home bucket, then the next one only when it is full
-    // (their nodes hold few keys; a second load per record cost more than
-    // the rare overflow)
+    // the home bucket, then the next one only when it is full (a second
+    // candidate bucket read for every record was measured slower: the
+    // fold is bound by shared-memory wavefronts, and at load <= 0.3 / small
+    // key counts the overflow it avoids is rare)
     constexpr uint32_t W = Sh::kW;
-    constexpr bool kTwo = sizeof(K) == 4;
-    const uint32_t b1 = home(k), b2 = kTwo ? home2(k, b1) : (b1 + 1) & (NB - 1);
+    const uint32_t b1 = home(k), b2 = (b1 + 1) & (NB - 1);
     TK q1[W], q2[W];
     bucket_keys(tk, b1, q1);
     uint32_t slot = T, e1 = W, e2 = W;
-    if constexpr (kTwo) bucket_keys(tk, b2, q2);
 #pragma unroll
     for (int i = W - 1; i >= 0; --i) {
       if (q1[i] == k) slot = W * b1 + i;
       if (q1[i] == kEmpty) e1 = i;
-      if constexpr (kTwo) {
+    }
+    if (slot == T && e1 == W) {   // home bucket full: read the next one
+      bucket_keys(tk, b2, q2);
+#pragma unroll
+      for (int i = W - 1; i >= 0; --i) {
         if (q2[i] == k) slot = W * b2 + i;
         if (q2[i] == kEmpty) e2 = i;
-      }
-    }
-    if constexpr (!kTwo) {
-      if (slot == T && e1 == W) {   // home bucket full: read the next one
-        bucket_keys(tk, b2, q2);
-#pragma unroll
-        for (int i = W - 1; i >= 0; --i) {
-          if (q2[i] == k) slot = W * b2 + i;
-          if (q2[i] == kEmpty) e2 = i;
-        }
       }
     }
     if (slot == T) {   // absent (or beyond both buckets): one inline claim attempt
