@@ -65,15 +65,19 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restric
     const uint32_t len = wk.len;
     const uint32_t nl = bf.n_light;
     uint32_t done = 0;
-    if constexpr (!SUM && (sizeof(K) == 4 || sizeof(K) == 8)) {
-      // counting: 16-byte key loads and packed id stores over the aligned
+    // values matter only for heavy records (their partial sums): a node
+    // without heavy keys (c3's root) never reads its value column here
+    const bool need_v = SUM && nd.n_heavy > 0;
+    if constexpr (sizeof(K) == 4 || sizeof(K) == 8) {
+      // keys only: 16-byte key loads and packed id stores over the aligned
       // full batches (work items start at multiples of 8 records)
       constexpr uint32_t V = 16 / sizeof(K), NV = kCountItems / V, kBatch = kCountThreads * kCountItems;
       using VT = std::conditional_t<sizeof(K) == 8, ulonglong2, uint4>;
       using IT = std::conditional_t<V == 2, uint32_t, uint2>;
       const K* ws = src + begin;
       uint16_t* wids = ids_out + begin;
-      if (ss == 1 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 && (reinterpret_cast<uintptr_t>(wids) & (2 * V - 1)) == 0) {
+      if (!need_v && ss == 1 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
+          (reinterpret_cast<uintptr_t>(wids) & (2 * V - 1)) == 0) {
         done = len - len % kBatch;
         for (uint32_t base = 0; base < done; base += kBatch) {
           VT kv[NV];
@@ -106,7 +110,7 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restric
       for (int k = 0; k < kCountItems; ++k) {
         uint32_t i = base + k * kCountThreads + threadIdx.x;
         keys[k] = i < len ? ldg_key(src, (begin + i) * ss) : K(0);
-        if constexpr (SUM) vals[k] = i < len ? val_u64(sv[(begin + i) * ss]) : 0ull;
+        if constexpr (SUM) vals[k] = need_v && i < len ? val_u64(sv[(begin + i) * ss]) : 0ull;
       }
 #pragma unroll
       for (int k = 0; k < kCountItems; ++k) {
