@@ -383,3 +383,25 @@ def test_node_fold_vs_oracle_and_level_path(S, case, monkeypatch):
         assert np.array_equal(k1, k2) and np.array_equal(a1, a2)
     if name == "u16_wrap":   # the hot key's node folds with 32-bit sum-side counts, not with 16-bit ones
         assert folded["count"] == folded["sum64"] - 1, folded
+
+
+# ---- leaf size classes ---------------------------------------------------------------
+
+@pytest.mark.parametrize("kdt", [np.uint32, np.uint64])
+@pytest.mark.parametrize("lb,alpha", [(512, 16384), (64, 65536)])
+def test_leaf_classes_vs_oracle(S, kdt, lb, alpha):
+    """Mid-size leaves (1025..4096 records: shared-memory k_leaf_eq_mid) and
+    larger ones (global scratch) reproduce the reference order byte for
+    byte; u32 keys also run the 8192-record distribute tiles."""
+    rng = np.random.default_rng(17)
+    n = 1 << 21
+    keys = rng.integers(0, 1 << 20, n).astype(kdt)
+    vals = np.arange(n, dtype=np.uint64)
+    kw = {"light_buckets": lb, "base_case_cutoff": alpha}
+    ko, vo, tel_o = O.semisort(keys, vals, O.OracleParams.derive(n, **kw))
+    data = S.RecordArray(keys, vals)
+    tel = S.Telemetry()
+    S.semisort(data, S.UIntKeyAdapter(), "eq", S.TuningParams.for_input(n, **kw), telemetry=tel)
+    assert np.array_equal(data.values_host(), vo) and np.array_equal(data.keys_host(), ko)
+    assert tel.max_depth == tel_o.max_depth and tel.nodes == tel_o.nodes
+    assert tel.leaves_global > 0   # the mid / global class ran
