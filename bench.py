@@ -394,6 +394,61 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def multi_e2e(args, S, src, work, adp, dist_semisort, barrier, dev, n, world):
+    """e2e at N > 1 GPUs (see the comment inside); never fails the bench line:
+    an error is reported in the e2e object instead."""
+    import torch
+    import torch.distributed as dist
+    try:
+        # per rank: its pinned host shard -> dist_semisort (partition, NCCL
+        # exchange, local semisort) -> its output shard back to pinned host;
+        # max over ranks.  The shard is capped at 2.5e8 records per rank to
+        # bound pinned host memory (8 ranks x 9 GB); "n" says what ran.
+        en = args.e2e_n or min(n, 250_000_000)
+        hk = torch.empty(en, dtype=torch.uint64, pin_memory=True)
+        hv = torch.empty(en, dtype=torch.uint64, pin_memory=True)
+        cap = en + en // 4 + 1024
+        ok = torch.empty(cap, dtype=torch.uint64, pin_memory=True)
+        ov = torch.empty(cap, dtype=torch.uint64, pin_memory=True)
+        hk.copy_(src.keys[:en])
+        hv.copy_(src.values[:en])
+        del work
+        torch.cuda.empty_cache()
+        ts, moved_out = [], 0
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            torch.cuda.synchronize()
+            barrier()
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            data = S.RecordArray(hk, hv)
+            res = dist_semisort(data, adp, args.mode)
+            m_out = len(res)
+            if m_out > cap:
+                raise RuntimeError("received shard larger than the pinned output buffer")
+            ok[:m_out].copy_(res.keys, non_blocking=True)
+            ov[:m_out].copy_(res.values, non_blocking=True)
+            e1.record(st)
+            torch.cuda.synchronize()
+            barrier()
+            if i:
+                ts.append(e0.elapsed_time(e1))
+                moved_out = m_out
+            del data, res
+        tt = torch.tensor([sum(ts) / len(ts)], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = float(tt.item())
+        e2e = {"value": en * world / (e_ms / 1e3) / 1e9, "unit": "Grecords/s", "h2d_bytes_per_step": 16 * en * world,
+               "d2h_bytes_per_step": 16 * en * world, "ms_per_step": e_ms, "n": en * world,
+               "path": "per rank: RecordArray(pinned host shard) -> dist_semisort (NCCL all_to_all_v) -> "
+                       "output shard to pinned host; max over ranks; bytes summed over ranks (rank 0 moved "
+                       f"{moved_out} records out)"}
+
+        return e2e
+    except Exception as exc:   # untested multi-GPU leg: report, keep the main line
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -542,6 +597,8 @@ def main():
         e2e = {"value": en / (e_ms / 1e3) / 1e9, "unit": "Grecords/s", "h2d_bytes_per_step": 16 * en,
                "d2h_bytes_per_step": 16 * en, "ms_per_step": e_ms, "n": en,
                "path": "RecordArray(pinned host tensors) -> semisort -> copy to pinned host"}
+    elif not args.no_e2e and world > 1:
+        e2e = multi_e2e(args, S, src, work, adp, dist_semisort, barrier, dev, n, world)
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
