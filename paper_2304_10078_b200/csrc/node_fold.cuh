@@ -19,7 +19,7 @@
 // child is < alpha (a child >= alpha would recurse, aggregate.py:139-141)
 // and its distinct keys fit the table; otherwise it reports failure and
 // takes the regular level path (the table is discarded, nothing was
-// written).
+// written; u32 counting also falls back when a 16-bit count wrapped).
 //
 // Table: buckets of 16 bytes (4 u32 or 2 u64 slots), one shared load each;
 // a key's home bucket is a multiplicative fold of the raw key (independent
@@ -34,8 +34,8 @@
 // (home bucket, key) -- a counting sort over home buckets, then a key sort
 // inside each (small) home group in the L2-resident staging area.
 //
-// Roofline: one read of the node's records (K [+ V] bytes each) plus the
-// pairs -- HBM bound when the table probes stay in shared memory.
+// Algorithmic bytes: one read of the node's records (K [+ V] bytes each)
+// plus the pairs; measured bound: shared-memory wavefronts (above).
 #pragma once
 
 #include <type_traits>
