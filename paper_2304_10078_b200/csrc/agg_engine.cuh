@@ -639,9 +639,9 @@ struct AggEngine {
     uint64_t R = 0;
     for (auto& nd : cur) R += nd.size;
     const uint64_t chunk = (std::max<uint64_t>(kMinChunk, cdiv(R, kTargetRows)) + 7) & ~uint64_t(7);   // aligned items
-    uint64_t max_nrows = 0;   // rows per scan group: <= 64 groups per node (see SortEngine::level)
+    uint64_t max_nrows = 0;   // rows per scan group: <= 128 groups per node (see SortEngine::level)
     for (auto& nd : cur) max_nrows = std::max<uint64_t>(max_nrows, cdiv(nd.size, chunk));
-    const uint32_t rg = static_cast<uint32_t>(std::max<uint64_t>(kRowGroup, cdiv(max_nrows, 64)));
+    const uint32_t rg = static_cast<uint32_t>(std::max<uint64_t>(kRowGroup, cdiv(max_nrows, 128)));
     std::vector<Work> work;
     std::vector<uint32_t> grp_node;
     for (uint32_t j = 0; j < nn; ++j) {
