@@ -32,6 +32,10 @@
  *   ss_distribute          core.py:339-380      distribute(...) / _distribute_ids(...)
  *   ss_base_case           core.py:404-429      base_case_eq / base_case_lt
  *   ss_partition           (new, multi-GPU)     stable hash partition before the exchange
+ *   ss_partition_pairs     (new, multi-GPU)     the same, packed records for ONE exchange
+ *   ss_semisort_pairs      core.py:566-598      semisort of received packed records, in place
+ *   ss_dist_semisort       (new, multi-GPU)     one rank of the sharded semisort over NCCL
+ *   ss_params_for_input    params.py:64-86      TuningParams.for_input for a rank's size
  */
 #ifndef SEMISORT_B200_H
 #define SEMISORT_B200_H
@@ -184,6 +188,60 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
                  uint64_t* out_counts, void* workspace, uint64_t workspace_bytes, void* stream);
 uint64_t ss_partition_workspace_bytes(uint64_t n, uint32_t parts);
 
+/* Packed variant (one exchange instead of one per column): keys and values
+ * of the key width (4 or 8 bytes) are written to dst_pairs as (key, value)
+ * records, 2n words, grouped by part in stable order. */
+int ss_partition_pairs(const void* keys, const void* values, uint64_t n, uint32_t key_bytes,
+                       uint32_t parts, void* dst_pairs, uint64_t* out_counts, void* workspace,
+                       uint64_t workspace_bytes, void* stream);
+uint64_t ss_partition_pairs_workspace_bytes(uint64_t n, uint32_t parts);
+
+/* Semisort of n packed (key, value) records (what a rank receives from the
+ * exchange).  The result is left as SoA columns in the SAME memory:
+ * keys = words [0, n), values = words [n, 2n) of `pairs`.  scratch: 2n
+ * words (e.g. the partition's send buffer, free after the exchange), or
+ * NULL to carve it from the workspace (ss_semisort_pairs_workspace_bytes
+ * with_scratch = 1).  Otherwise as ss_semisort (core.py:566-598). */
+int ss_semisort_pairs(void* pairs, uint64_t n, uint32_t key_bytes, int mode, int identity,
+                      const ss_params* params, void* scratch, void* workspace, uint64_t workspace_bytes,
+                      ss_telemetry* telemetry, void* stream);
+uint64_t ss_semisort_pairs_workspace_bytes(uint64_t n, uint32_t key_bytes, const ss_params* params,
+                                           int with_scratch);
+
+/* TuningParams.for_input(n, ...) (params.py:64-86) with the tunables of
+ * `tmpl`: subarray_len, sample_count and the heavy threshold re-derived
+ * for n (a rank's received size is known only after the count exchange). */
+int ss_params_for_input(uint64_t n, const ss_params* tmpl, ss_params* out);
+
+/* ---- multi-GPU over NCCL (new, the reference has no
+ * distributed path).  NCCL is loaded at run time (libnccl.so.2).  One
+ * process per GPU; the caller sets the device before ss_nccl_comm_init.
+ * ss_dist_semisort runs one rank's whole pipeline on `stream`:
+ *   1. stable packed partition by dest = top log2(world) bits of mix64(key)
+ *      into `scratch` (2 * capacity words),
+ *   2. per-peer counts exchanged (grouped ncclSend / ncclRecv),
+ *   3. ONE all-to-allv of packed records into `recv_block` (2 * capacity
+ *      words), in source-rank order,
+ *   4. ss_semisort_pairs of what arrived (params re-derived for that size
+ *      from `params`' tunables), scratch reused.
+ * Output: *out_n records, keys = recv_block words [0, *out_n), values =
+ * words [*out_n, 2 * *out_n).  recv_block may alias the input columns
+ * (the partition has consumed them before anything is received), which is
+ * what lets strong scaling keep two buffers per rank.  If more than
+ * `capacity` records would arrive the call fails with SS_ERR_RESOURCE
+ * before the payload exchange (the input is intact, *out_n says how many).
+ * The rank-ordered concatenation of every rank's output is a stable
+ * global semisort. */
+int ss_nccl_unique_id(unsigned char* out128);
+int ss_nccl_comm_init(const unsigned char* id128, int world, int rank, void** out_comm);
+int ss_nccl_comm_destroy(void* comm);
+int ss_dist_semisort(void* comm, uint32_t world, uint32_t rank, const void* keys, const void* values,
+                     uint64_t n_local, uint32_t key_bytes, int mode, int identity, const ss_params* params,
+                     void* recv_block, void* scratch, uint64_t capacity, void* workspace,
+                     uint64_t workspace_bytes, uint64_t* out_n, ss_telemetry* telemetry, void* stream);
+uint64_t ss_dist_semisort_workspace_bytes(uint64_t capacity, uint32_t key_bytes, uint32_t world,
+                                          const ss_params* params);
+
 /* ---- device utilities (bench / validation) ----------------------------- */
 
 /* Seeded synthetic keys with the reference generator families
@@ -205,6 +263,20 @@ int ss_validate_indexed(const void* keys_in, const void* keys_out, const void* v
                         uint64_t distinct_keys, void* workspace, uint64_t workspace_bytes,
                         int32_t* out_flags, void* stream);
 uint64_t ss_validate_workspace_bytes(uint64_t n);
+
+/* Validation of one output shard of a generated input (ss_generate family,
+ * param, universe, seed, hash_ranks) whose values are the global record
+ * indices: out[0] records whose key differs from the generator's key for
+ * their value, out[1] runs (key changes + 1), out[2] stability violations
+ * inside runs, out[3] keys whose dest (top log2(parts) bits of mix64) is not
+ * `rank`, out[4..6] sum of v, v^2, mix64(v) (mod 2^64) -- the ranks add the
+ * fingerprints and compare with ss_index_fingerprint over [0, N). */
+int ss_validate_shard(int family, double param, uint64_t universe, uint64_t seed, int hash_ranks,
+                      const void* keys_out, const void* values_out, uint64_t m, uint32_t key_bytes,
+                      uint32_t parts, uint32_t rank, void* workspace, uint64_t workspace_bytes,
+                      uint64_t* out7, void* stream);
+int ss_index_fingerprint(uint64_t lo, uint64_t hi, void* workspace, uint64_t workspace_bytes, uint64_t* out3,
+                         void* stream);
 
 /* Number of distinct keys (GPU hash set; the contiguity reference count). */
 int ss_count_distinct(const void* keys, uint64_t n, uint32_t key_bytes, void* workspace,

@@ -77,6 +77,21 @@ _SIGS = {
                                 C.POINTER(SSTelemetry), vp]),
     "ss_records_unpack": (i32, [vp, u64, u32, u32, vp, vp, vp]),
     "ss_records_pack": (i32, [vp, vp, u64, u32, u32, vp, vp]),
+    "ss_partition_pairs": (i32, [vp, vp, u64, u32, u32, vp, C.POINTER(u64), vp, u64, vp]),
+    "ss_partition_pairs_workspace_bytes": (u64, [u64, u32]),
+    "ss_semisort_pairs": (i32, [vp, u64, u32, i32, i32, C.POINTER(SSParams), vp, vp, u64,
+                                C.POINTER(SSTelemetry), vp]),
+    "ss_semisort_pairs_workspace_bytes": (u64, [u64, u32, C.POINTER(SSParams), i32]),
+    "ss_params_for_input": (i32, [u64, C.POINTER(SSParams), C.POINTER(SSParams)]),
+    "ss_nccl_unique_id": (i32, [C.c_char_p]),
+    "ss_nccl_comm_init": (i32, [C.c_char_p, i32, i32, C.POINTER(vp)]),
+    "ss_nccl_comm_destroy": (i32, [vp]),
+    "ss_dist_semisort": (i32, [vp, u32, u32, vp, vp, u64, u32, i32, i32, C.POINTER(SSParams), vp, vp, u64, vp,
+                               u64, C.POINTER(u64), C.POINTER(SSTelemetry), vp]),
+    "ss_dist_semisort_workspace_bytes": (u64, [u64, u32, u32, C.POINTER(SSParams)]),
+    "ss_validate_shard": (i32, [i32, C.c_double, u64, u64, i32, vp, vp, u64, u32, u32, u32, vp, u64,
+                                C.POINTER(u64), vp]),
+    "ss_index_fingerprint": (i32, [u64, u64, vp, u64, C.POINTER(u64), vp]),
 }
 
 EXPORTS = tuple(_SIGS)

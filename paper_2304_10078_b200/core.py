@@ -270,6 +270,17 @@ def get_bucket_id(key, heavy: HeavyTable | None, adapter: KeyAdapter, params: Tu
     return int(ids.item())
 
 
+def _check_ids(ids: torch.Tensor, n_buckets: int) -> None:
+    """Bucket ids must lie in [0, n_buckets): the kernels index shared-memory
+    counters by them (the reference rejects such ids in bincount / indexing)."""
+    if ids.numel() == 0:
+        return
+    lo, hi = torch.aminmax(ids)
+    lo, hi = int(lo.item()), int(hi.item())
+    if lo < 0 or hi >= n_buckets:
+        raise ConfigurationError(f"bucket ids must lie in [0, {n_buckets}); got [{lo}, {hi}]")
+
+
 def _counts(data: RecordArray, ids, params: TuningParams, n_buckets: int, heavy, adapter, depth):
     n = len(data) if data is not None else len(ids)
     dev = data.device if data is not None else ids.device
@@ -277,7 +288,10 @@ def _counts(data: RecordArray, ids, params: TuningParams, n_buckets: int, heavy,
     counts = torch.zeros((rows, n_buckets), dtype=torch.int64, device=dev)
     if n == 0:
         return counts
-    kb = data.key_bytes if data is not None else 8
+    # ids-only counting reads the 4-byte id column as u32 "keys"
+    kb = data.key_bytes if data is not None else 4
+    if ids is not None:
+        _check_ids(ids, n_buckets)
     hk, nh = _heavy_args(heavy, dev)
     ident = device_identity_flag(adapter) if adapter is not None else 0
     pc = params.as_c()
@@ -338,6 +352,8 @@ def _distribute(src: RecordArray, dst: RecordArray, ids, prefix, params: TuningP
     p = prefix.to(torch.int64).contiguous() if isinstance(prefix, torch.Tensor) else \
         torch.from_numpy(np.ascontiguousarray(np.asarray(prefix, dtype=np.int64)))
     p = p.to(dev)
+    if ids is not None:
+        _check_ids(ids, n_buckets)
     hk, nh = _heavy_args(heavy, dev)
     ident = device_identity_flag(adapter) if adapter is not None else 0
     pc = params.as_c()
@@ -364,11 +380,20 @@ def distribute(data: RecordArray, prefix, heavy: HeavyTable, adapter: KeyAdapter
 
 def distribute_ids(src: RecordArray, dst: RecordArray, base: int, ids, prefix, params: TuningParams,
                    n_buckets: int, pool=None) -> None:
-    """core.py:339-362 (_distribute_ids) for base == 0 windows."""
-    if base:
-        src, dst = src.view(base, len(src)), dst.view(base, len(dst))
+    """core.py:339-362 (_distribute_ids): move the node's records
+    src[base:base+len(ids)] to dst[base + cursor] (the window is len(ids)
+    records wide on both sides, as in the reference)."""
     ids = ids.to(torch.int32).contiguous() if isinstance(ids, torch.Tensor) else \
         torch.from_numpy(np.asarray(ids, dtype=np.int32)).to(src.device)
+    m = int(ids.shape[0])
+    base = int(base)
+    if base < 0 or base + m > len(src) or base + m > len(dst):
+        raise ConfigurationError(f"window [{base}, {base + m}) exceeds the source/destination arrays")
+    rows = params.num_subarrays(m)
+    pshape = tuple(prefix.shape) if hasattr(prefix, "shape") else np.asarray(prefix).shape
+    if m and pshape != (rows, n_buckets):
+        raise ConfigurationError(f"prefix has shape {pshape}, expected {(rows, n_buckets)}")
+    src, dst = src.view(base, base + m), dst.view(base, base + m)
     _distribute(src, dst, ids, prefix, params, n_buckets, None, None, 0)
 
 
@@ -461,3 +486,53 @@ def local_refine(buffers: WorkBuffers, plan: BucketPlan, adapter: KeyAdapter, mo
         offs.ctypes.data_as(C.POINTER(C.c_int64)), nb, 1 if buffers.live_in_primary else 0, depth,
         ws.data_ptr(), ws.numel(), C.byref(ct), _stream(dev)))
     tel._absorb(ct)
+
+
+def _raw(keys, values, kind) -> RecordArray:
+    r = RecordArray.__new__(RecordArray)
+    r.keys, r.values, r.arena, r.key_kind = keys, values, None, kind
+    return r
+
+
+def semisort_packed(pairs: torch.Tensor, n: int, adapter: KeyAdapter, mode: str = "eq",
+                    params: TuningParams | None = None, *, scratch: torch.Tensor | None = None,
+                    telemetry: Telemetry | None = None) -> RecordArray:
+    """Semisort of ``n`` packed (key, value) records held in the first 2n
+    words of ``pairs`` (uint32 or uint64; what a rank receives from the
+    multi-GPU exchange).  Same result and errors as ``semisort`` on the
+    unpacked columns (core.py:566-598); the result is left as SoA columns in
+    the same memory and returned as a RecordArray of views: keys = words
+    [0, n), values = words [n, 2n).  ``scratch`` (>= 2n words of the same
+    dtype, e.g. the exchange's send buffer) replaces the internal scratch."""
+    if mode not in ("eq", "lt"):
+        raise ConfigurationError(f"mode must be 'eq' or 'lt', got {mode!r}")
+    if mode == "lt" and not adapter.has_lt:
+        raise ContractError("mode 'lt' requires an adapter with a less-than test")
+    ident = device_identity_flag(adapter)
+    flat = pairs.reshape(-1)
+    if flat.dtype not in (torch.uint32, torch.uint64) or not flat.is_cuda or not flat.is_contiguous():
+        raise ContractError("packed records must be a contiguous uint32/uint64 CUDA tensor")
+    if flat.numel() < 2 * n:
+        raise ConfigurationError(f"{flat.numel()} words hold fewer than {n} packed records")
+    kb = flat.element_size()
+    params = _check_params(params, n)
+    tel = telemetry if telemetry is not None else Telemetry()
+    dev = flat.device
+    scr = None
+    if scratch is not None:
+        s = scratch.reshape(-1)
+        if s.dtype != flat.dtype or s.numel() < 2 * n or not s.is_contiguous():
+            raise ConfigurationError("scratch must hold 2n words of the records' dtype")
+        scr = s
+    pc = params.as_c()
+    lib = _lib.lib()
+    wsb = lib.ss_semisort_pairs_workspace_bytes(n, kb, C.byref(pc), 0 if scr is not None else 1)
+    if wsb == 0:
+        _lib.check(_lib.SS_ERR_CONFIG)
+    ws = _workspace(wsb, dev)
+    ct = tel._c()
+    _lib.check(lib.ss_semisort_pairs(flat.data_ptr(), n, kb, _lib.SS_MODE_LT if mode == "lt" else _lib.SS_MODE_EQ,
+                                     ident, C.byref(pc), _ptr(scr), ws.data_ptr(), ws.numel(), C.byref(ct),
+                                     _stream(dev)))
+    tel._absorb(ct)
+    return _raw(flat[:n], flat[n:2 * n], "u64" if kb == 8 else "u32")

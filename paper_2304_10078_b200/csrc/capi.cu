@@ -130,6 +130,27 @@ struct PhasePlan {
   }
 };
 
+// Caller-supplied bucket ids index shared-memory counters: reject any id
+// outside [0, nb) before a kernel uses it (the reference raises for them).
+__global__ void k_check_ids(const int32_t* ids, uint64_t n, uint32_t nb, uint32_t* bad) {
+  uint32_t local = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    local |= static_cast<uint32_t>(ids[i]) >= nb ? 1u : 0u;
+  if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(bad, 1u);
+}
+
+inline void check_ids(const void* ids, uint64_t n, uint32_t nb, uint32_t* d_flag, cudaStream_t st) {
+  SS_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(uint32_t), st));
+  k_check_ids<<<static_cast<uint32_t>(std::min<uint64_t>(cdiv(n, 256), 1184)), 256, 0, st>>>(
+      static_cast<const int32_t*>(ids), n, nb, d_flag);
+  check_launch();
+  uint32_t bad = 0;
+  SS_CUDA(cudaMemcpyAsync(&bad, d_flag, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  if (bad) throw Fail(SS_ERR_CONFIG, "bucket ids must lie in [0, n_buckets)");
+}
+
 __global__ void k_u32_to_i64(const uint32_t* src, uint64_t rows, uint32_t cols, uint32_t stride, int64_t* dst) {
   uint64_t total = rows * cols;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -464,6 +485,7 @@ int ss_count_matrix(const void* keys, const void* ids, uint64_t n, uint32_t key_
     pp.upload_single(n, depth, n_heavy, P.subarray_len, st, work, gn, nd);
     if (n_heavy)
       SS_CUDA(cudaMemcpyAsync(pp.d_heavy, heavy_keys, n_heavy * 8, cudaMemcpyDeviceToDevice, st));
+    if (ids) check_ids(ids, n, n_buckets, pp.d_ctr, st);
     dispatch_k(key_bytes, [&]<typename K>() {
       const uint32_t nw = static_cast<uint32_t>(work.size());
       if (ids) {
@@ -549,6 +571,7 @@ int ss_distribute(const void* src_keys, const void* src_values, void* dst_keys, 
     k_i64_to_u64_strided<<<grid_for(nd.n_rows * static_cast<uint64_t>(n_buckets)), 256, 0, st>>>(
         static_cast<const int64_t*>(prefix), nd.n_rows, n_buckets, pp.stride, pp.d_X);
     check_launch();
+    if (ids) check_ids(ids, n, n_buckets, pp.d_ctr, st);
     const uint32_t nw = static_cast<uint32_t>(work.size());
     dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
       // bucket ids (u16) by the count kernel, then the stable scatter

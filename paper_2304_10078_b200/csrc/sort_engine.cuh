@@ -243,6 +243,11 @@ struct SortEngine {
   uint32_t* d_leafscr = nullptr;
   uint16_t* d_ids = nullptr;   // per-record bucket ids of the current level
   bool external_scratch = false;
+  // Root source in the pair layout (ss_semisort_pairs): level 1 reads the
+  // (key, value) records at R_pairs instead of A; A aliases that memory as
+  // SoA columns and is first written by the root's heavy copy-back, after the
+  // level-1 distribute has consumed every record of R (stream order).
+  const K* R_pairs = nullptr;
 
   void plan(Arena& a, bool carve_scratch = true) {
     stride = even_stride(P);
@@ -416,8 +421,9 @@ struct SortEngine {
   // ---- one recursion level -------------------------------------------------
   std::vector<Node> level(Tracker& tr, std::vector<Node>& cur, int lvl, bool flip) {
     const bool from_a = src_is_A(lvl, flip);
-    const K* sk = from_a ? A_k : S_k;
-    const V* sv = from_a ? A_v : S_v;
+    const bool from_r = R_pairs && lvl == 1 && !flip;   // root of ss_semisort_pairs
+    const K* sk = from_r ? R_pairs : from_a ? A_k : S_k;
+    const V* sv = from_r ? reinterpret_cast<const V*>(R_pairs + 1) : from_a ? A_v : S_v;
     K* dk = from_a ? S_k : A_k;
     V* dv = from_a ? S_v : A_v;
     const uint32_t nn = static_cast<uint32_t>(cur.size());
@@ -463,7 +469,7 @@ struct SortEngine {
     // sampling + heavy tables
     tr.begin(kPhSample);
     SS_CUDA(cudaFuncSetAttribute(k_sample<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSampleSmem)));
-    const uint32_t kss = from_a ? 1u : s_ss();   // key stride of the source side
+    const uint32_t kss = from_r ? 2u : from_a ? 1u : s_ss();   // key stride of the source side
     k_sample<K><<<std::min<uint32_t>(sample_grid, nn), kSampleThreads, kSampleSmem, st>>>(
         sk, d_nodes, nn, d_heavy, d_samp, s_cap, P, 0, 0, kss);
     check_launch();
@@ -500,7 +506,7 @@ struct SortEngine {
     // even levels (A -> S, copied back): heavy keys are filled by the copy
     launch_distribute<K, V>(sk, sv, d_ids, dk, dv, d_work, nwork, d_nodes, d_X, stride, 0xFFFFFFFFu,
                             P.light_buckets, 0, st, n, d_ctr, from_a ? P.light_buckets : 0xFFFFFFFFu,
-                            aos && !from_a, aos && from_a);
+                            from_r || (aos && !from_a), aos && from_a);
     check_launch();
     tr.launched();
 

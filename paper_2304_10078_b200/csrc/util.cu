@@ -11,6 +11,7 @@
 
 #include "engine.cuh"
 #include "multisplit.cuh"
+#include "partition.cuh"
 
 namespace ss {
 
@@ -76,45 +77,102 @@ __device__ inline uint64_t zipf_draw(const ZipfCfg& z, uint64_t key, uint64_t ct
   }
 }
 
+// Key of global record g (a pure function of g: any shard, or any single
+// record, regenerates independently).
+__device__ inline uint64_t gen_key(int family, double param, const ZipfCfg& z, uint64_t kkey, int hash_ranks,
+                                   uint64_t g) {
+  U64x4 r = philox4x64_10(g + 1, kkey);
+  switch (family) {
+    case 0: {   // uniform [0, param)
+      uint64_t hi, lo;
+      mulhilo64(r.v[0], static_cast<uint64_t>(param), hi, lo);
+      return hi;
+    }
+    case 1:     // floor(exponential(scale = 1/param))
+      return static_cast<uint64_t>(floor(-log1p(-u01(r.v[0])) / param));
+    case 2: {   // zipf rank in [1, universe]
+      const uint64_t k = zipf_draw(z, kkey ^ 0x5A5Aull, g + 1);
+      return hash_ranks ? mix64(k - 1) : k;
+    }
+    case 3:
+      return r.v[0];
+    default:    // config-5 mix: uniform 64-bit or zipf(param) rank - 1
+      return (r.v[1] & 1) ? r.v[0] : zipf_draw(z, kkey ^ 0x5A5Aull, g + 1) - 1;
+  }
+}
+
+__host__ __device__ inline uint64_t gen_kkey(uint64_t seed, int family) { return mix64_pair(seed, 0xA11CEull + family); }
+
 template <typename K, typename V>
 __global__ void k_generate(int family, double param, uint64_t universe, uint64_t n, uint64_t first, uint64_t seed,
                            int hash_ranks, ZipfCfg z, K* __restrict__ keys, V* __restrict__ vals, int values_mode,
                            uint32_t value_shift) {
-  const uint64_t kkey = mix64_pair(seed, 0xA11CEull + family);
+  const uint64_t kkey = gen_kkey(seed, family);
   const uint64_t vkey = mix64_pair(seed, 0xB0Bull);
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t g = first + i;
-    U64x4 r = philox4x64_10(g + 1, kkey);
-    uint64_t k;
-    switch (family) {
-      case 0: {   // uniform [0, param)
-        uint64_t hi, lo;
-        mulhilo64(r.v[0], static_cast<uint64_t>(param), hi, lo);
-        k = hi;
-        break;
-      }
-      case 1:     // floor(exponential(scale = 1/param))
-        k = static_cast<uint64_t>(floor(-log1p(-u01(r.v[0])) / param));
-        break;
-      case 2:     // zipf rank in [1, universe]
-        k = zipf_draw(z, kkey ^ 0x5A5Aull, g + 1);
-        if (hash_ranks) k = mix64(k - 1);
-        break;
-      case 3:
-        k = r.v[0];
-        break;
-      default:    // config-5 mix: uniform 64-bit or zipf(param) rank - 1
-        k = (r.v[1] & 1) ? r.v[0] : zipf_draw(z, kkey ^ 0x5A5Aull, g + 1) - 1;
-        break;
-    }
-    keys[i] = static_cast<K>(k);
+    keys[i] = static_cast<K>(gen_key(family, param, z, kkey, hash_ranks, g));
     if (values_mode == 1) {
       vals[i] = static_cast<V>(g);
     } else if (values_mode == 2) {
       U64x4 q = philox4x64_10(g + 1, vkey);
       vals[i] = static_cast<V>(q.v[0] >> value_shift);
     }
+  }
+}
+
+// Shard validation for generated inputs whose value is the global record
+// index: record integrity against the generator itself
+// (key_out[i] == key(value_out[i])), stability inside runs, dest(key) ==
+// rank (top `bits` of mix64), run count, and the permutation fingerprints
+// count / sum v / sum v^2 / sum mix64(v) (mod 2^64) that the ranks add up
+// and compare with those of [0, N).
+// acc: [0] bad record, [1] runs, [2] bad stability, [3] bad dest,
+//      [4] sum v, [5] sum v^2, [6] sum mix64(v)
+template <typename K>
+__global__ void k_validate_shard(int family, double param, ZipfCfg z, uint64_t kkey, int hash_ranks,
+                                 const K* __restrict__ ko, const uint64_t* __restrict__ vo, uint64_t m,
+                                 uint32_t bits, uint32_t rank, unsigned long long* __restrict__ acc) {
+  unsigned long long c[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = vo[i];
+    const K k = ko[i];
+    c[0] += static_cast<K>(gen_key(family, param, z, kkey, hash_ranks, v)) != k;
+    if (i == 0 || ko[i - 1] != k) ++c[1];
+    else c[2] += vo[i - 1] >= v;
+    if (bits) c[3] += static_cast<uint32_t>(mix64(static_cast<uint64_t>(k)) >> (64 - bits)) != rank;
+    c[4] += v;
+    c[5] += v * v;
+    c[6] += mix64(v);
+  }
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    unsigned long long x = c[j];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&acc[j], x);
+  }
+}
+
+// The same fingerprints over the index range [lo, hi).
+__global__ void k_index_fingerprint(uint64_t lo, uint64_t hi, unsigned long long* __restrict__ acc) {
+  unsigned long long a = 0, b = 0, c = 0;
+  for (uint64_t v = lo + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < hi;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    a += v;
+    b += v * v;
+    c += mix64(v);
+  }
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&acc[0], a);
+    atomicAdd(&acc[1], b);
+    atomicAdd(&acc[2], c);
   }
 }
 
@@ -185,51 +243,6 @@ __global__ void k_count_distinct(const K* __restrict__ keys, uint64_t n, uint64_
 // partition by the top bits of mix64(key)
 // ---------------------------------------------------------------------------
 
-struct PartBuckets {
-  uint32_t shift;   // 64 - log2(parts); 64 means a single part
-  uint32_t nb;
-  template <typename T>
-  __device__ __forceinline__ void prepare(const Node&, uint32_t, T*) { __syncthreads(); }
-  __device__ __forceinline__ uint32_t n_buckets() const { return nb; }
-  __device__ __forceinline__ uint32_t first_hot() const { return nb; }
-  template <typename K>
-  __device__ __forceinline__ uint32_t operator()(K key, uint64_t) const {
-    return shift >= 64 ? 0u : static_cast<uint32_t>(mix64(static_cast<uint64_t>(key)) >> shift);
-  }
-  template <typename K, typename T>
-  __device__ __forceinline__ uint32_t operator()(K key, uint64_t pos, const T&) const {
-    return (*this)(key, pos);
-  }
-};
-
-struct PartPlan {
-  uint64_t rows, grps;
-  uint32_t stride;
-  Node* d_node;
-  Work* d_work;
-  uint32_t* d_gn;
-  uint32_t* d_C;
-  uint64_t* d_X;
-  uint64_t* d_P;
-  uint64_t* d_off;
-  uint16_t* d_ids;
-  uint32_t* d_ctr;
-  void carve(Arena& a, uint64_t n, uint32_t parts) {
-    stride = (parts + 1) & ~1u;
-    rows = std::max<uint64_t>(1, std::min<uint64_t>(1184, cdiv(n, 4096)));
-    grps = cdiv(rows, kRowGroup) + 1;
-    d_node = a.take<Node>(1);
-    d_work = a.take<Work>(rows);
-    d_gn = a.take<uint32_t>(grps);
-    d_C = a.take<uint32_t>(rows * stride);
-    d_X = a.take<uint64_t>(rows * stride);
-    d_P = a.take<uint64_t>(grps * stride);
-    d_off = a.take<uint64_t>(stride + 1);
-    d_ids = a.take<uint16_t>(n);
-    d_ctr = a.take<uint32_t>(4);
-  }
-};
-
 inline uint32_t ugrid(uint64_t n) {
   return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 16, cdiv(n, 256))));
 }
@@ -269,6 +282,58 @@ int ss_generate(int family, double param, uint64_t universe, uint64_t n, uint64_
       throw Fail(SS_ERR_CONTRACT, "key_bytes must be 4 or 8");
     }
     check_launch();
+  });
+}
+
+int ss_validate_shard(int family, double param, uint64_t universe, uint64_t seed, int hash_ranks,
+                      const void* keys_out, const void* values_out, uint64_t m, uint32_t key_bytes, uint32_t parts,
+                      uint32_t rank, void* workspace, uint64_t workspace_bytes, uint64_t* out, void* stream) {
+  return guarded_u([&] {
+    if (family < 0 || family > 4) throw Fail(SS_ERR_CONFIG, "unknown family");
+    if (parts < 1 || (parts & (parts - 1)) || rank >= parts) throw Fail(SS_ERR_CONFIG, "bad parts / rank");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Arena a(workspace, workspace_bytes);
+    unsigned long long* acc = a.take<unsigned long long>(8);
+    SS_CUDA(cudaMemsetAsync(acc, 0, 8 * 8, st));
+    uint32_t bits = 0;
+    while ((1u << bits) < parts) ++bits;
+    ZipfCfg z = make_zipf((family == 2 || family == 4) ? param : 1.2, std::max<uint64_t>(universe, 2));
+    const uint64_t kkey = gen_kkey(seed, family);
+    if (m) {
+      if (key_bytes == 8)
+        k_validate_shard<uint64_t><<<ugrid(m), 256, 0, st>>>(family, param, z, kkey, hash_ranks,
+                                                             static_cast<const uint64_t*>(keys_out),
+                                                             static_cast<const uint64_t*>(values_out), m, bits, rank, acc);
+      else if (key_bytes == 4)
+        k_validate_shard<uint32_t><<<ugrid(m), 256, 0, st>>>(family, param, z, kkey, hash_ranks,
+                                                             static_cast<const uint32_t*>(keys_out),
+                                                             static_cast<const uint64_t*>(values_out), m, bits, rank, acc);
+      else
+        throw Fail(SS_ERR_CONTRACT, "key_bytes must be 4 or 8");
+      check_launch();
+    }
+    unsigned long long h[8];
+    SS_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < 7; ++j) out[j] = h[j];
+  });
+}
+
+int ss_index_fingerprint(uint64_t lo, uint64_t hi, void* workspace, uint64_t workspace_bytes, uint64_t* out,
+                         void* stream) {
+  return guarded_u([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Arena a(workspace, workspace_bytes);
+    unsigned long long* acc = a.take<unsigned long long>(4);
+    SS_CUDA(cudaMemsetAsync(acc, 0, 4 * 8, st));
+    if (hi > lo) {
+      k_index_fingerprint<<<ugrid(hi - lo), 256, 0, st>>>(lo, hi, acc);
+      check_launch();
+    }
+    unsigned long long h[4];
+    SS_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < 3; ++j) out[j] = h[j];
   });
 }
 
@@ -357,38 +422,11 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
       for (uint32_t p = 0; p < parts; ++p) out_counts[p] = 0;
       return;
     }
-    uint32_t bits = 0;
-    while ((1u << bits) < parts) ++bits;
-    PartBuckets bf{64u - bits, parts};
-    const uint64_t chunk = cdiv(n, pp.rows);
     Node nd{};
-    nd.lo = 0;
-    nd.size = n;
-    nd.out_base = 0;
-    nd.n_rows = static_cast<uint32_t>(cdiv(n, chunk));
-    nd.n_grps = static_cast<uint32_t>(cdiv(nd.n_rows, kRowGroup));
-    std::vector<Work> work(nd.n_rows);
-    for (uint32_t r = 0; r < nd.n_rows; ++r) {
-      work[r].begin = r * chunk;
-      work[r].len = static_cast<uint32_t>(std::min<uint64_t>(chunk, n - r * chunk));
-      work[r].node = 0;
-      work[r].row = r;
-    }
-    std::vector<uint32_t> gn(nd.n_grps, 0);
-    SS_CUDA(cudaMemcpyAsync(pp.d_node, &nd, sizeof(Node), cudaMemcpyHostToDevice, st));
-    SS_CUDA(cudaMemcpyAsync(pp.d_work, work.data(), work.size() * sizeof(Work), cudaMemcpyHostToDevice, st));
-    SS_CUDA(cudaMemcpyAsync(pp.d_gn, gn.data(), gn.size() * 4, cudaMemcpyHostToDevice, st));
-    const uint32_t nw = nd.n_rows;
+    const uint32_t nw = partition_count_scan(pp, keys, n, key_bytes, parts, nd, st);
     auto go = [&](auto kt, auto vt) {
       using K = decltype(kt);
       using V = decltype(vt);
-      k_count<K, PartBuckets><<<nw, kCountThreads, pp.stride * 4, st>>>(static_cast<const K*>(keys), pp.d_work, nw,
-                                                                      pp.d_node, pp.d_C, pp.stride, bf, pp.d_ids);
-      k_colsum_groups<uint32_t><<<nd.n_grps, 256, 0, st>>>(pp.d_C, pp.d_node, pp.d_gn, nd.n_grps, pp.d_P, pp.stride, 0, 0,
-                                                           parts);
-      k_scan_nodes<<<1, 1024, 0, st>>>(pp.d_node, 1, pp.d_P, pp.d_off, pp.stride, 0, 0, parts, nullptr);
-      k_write_X<uint32_t, uint64_t><<<nd.n_grps, 256, 0, st>>>(pp.d_C, pp.d_node, pp.d_gn, nd.n_grps, pp.d_P, pp.d_X,
-                                                                pp.stride, 0, 0, parts, nullptr);
       constexpr int kTile = 2048;   // parts <= 4096 always fit this tile
       const size_t dsm = DistCfg<K, V, kTile, 512, 2>::smem_bytes(pp.stride);
       auto kern = k_distribute<K, V, kTile, 512, 2, false>;
@@ -411,10 +449,7 @@ int ss_partition(const void* keys, const void* values, uint64_t n, uint32_t key_
     if (key_bytes == 8) withv(uint64_t{});
     else withv(uint32_t{});
     check_launch();
-    std::vector<uint64_t> off(parts + 1);
-    SS_CUDA(cudaMemcpyAsync(off.data(), pp.d_off, (parts + 1) * 8, cudaMemcpyDeviceToHost, st));
-    SS_CUDA(cudaStreamSynchronize(st));
-    for (uint32_t p = 0; p < parts; ++p) out_counts[p] = off[p + 1] - off[p];
+    partition_counts(pp, parts, out_counts, st);
   });
 }
 

@@ -58,7 +58,30 @@ def cpu_reduce(data, spec, params):
     return KeyedResult(key_tensor=torch.from_numpy(ks), agg_tensor=torch.from_numpy(vs))
 
 
-def _worker(rank, world, port, q):
+def cpu_pack(data, parts, out=None):
+    """ss_partition_pairs semantics: stable partition into packed (key, value) words."""
+    grouped, counts = cpu_partition(data, parts)
+    n = len(grouped.keys)
+    words = torch.empty(2 * n, dtype=grouped.keys.dtype) if out is None else out
+    w = words.numpy() if out is None else words.numpy()
+    w[0:2 * n:2] = grouped.keys.numpy()
+    w[1:2 * n:2] = grouped.values.numpy()
+    return words, counts
+
+
+def cpu_sort_packed(words, m, params, scratch):
+    """ss_semisort_pairs semantics: semisort m packed records, leave SoA in place."""
+    from paper_2304_10078_b200.core import _raw
+    w = words.numpy()
+    k, v = w[0:2 * m:2].copy(), w[1:2 * m:2].copy()
+    P = O.OracleParams.derive(m, base_case_cutoff=256)
+    ko, vo, _ = O.semisort(k, v, P)
+    w[:m] = ko
+    w[m:2 * m] = vo
+    return _raw(words[:m], words[m:2 * m], "u64")
+
+
+def _worker(rank, world, port, q, packed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -71,9 +94,13 @@ def _worker(rank, world, port, q):
         offset = sum(3000 + 517 * r for r in range(rank))
         vals = np.arange(offset, offset + n_local, dtype=np.uint64)
         data = _ra(torch.from_numpy(keys.copy()), torch.from_numpy(vals))
-        out = dist_semisort(data, partitioner=cpu_partition, local_sort=cpu_sort)
-        hist = dist_histogram(_ra(torch.from_numpy(keys.copy()), None), partitioner=cpu_partition,
-                              local_reduce=cpu_reduce)
+        if packed:   # one exchange of packed records, sort from the packed receive buffer
+            out = dist_semisort(data, pack=cpu_pack, sort_packed=cpu_sort_packed)
+            hist = dist_histogram(_ra(torch.from_numpy(keys.copy()), None), pack=cpu_pack, local_reduce=cpu_reduce)
+        else:
+            out = dist_semisort(data, partitioner=cpu_partition, local_sort=cpu_sort)
+            hist = dist_histogram(_ra(torch.from_numpy(keys.copy()), None), partitioner=cpu_partition,
+                                  local_reduce=cpu_reduce)
         gathered = [None] * world
         dist.all_gather_object(gathered, (keys, out.keys.numpy(), out.values.numpy(),
                                           hist.key_tensor.numpy(), hist.agg_tensor.numpy()))
@@ -83,12 +110,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_dist_semisort_and_histogram_gloo(world):
+@pytest.mark.parametrize("world,packed", [(2, False), (4, False), (2, True), (4, True)])
+def test_dist_semisort_and_histogram_gloo(world, packed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, packed)) for r in range(world)]
     for p in procs:
         p.start()
     gathered = q.get(timeout=240)
