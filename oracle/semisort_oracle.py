@@ -24,7 +24,7 @@ __all__ = [
     "M64", "mix64_int", "mix64_np", "mix64_pair_int", "OracleParams",
     "OracleTelemetry", "key_hash", "light_slice", "sample_heavy",
     "bucket_ids", "count_rows", "col_scan", "scatter_positions",
-    "eq_leaf_order", "lt_leaf_order", "semisort", "collect_reduce",
+    "eq_leaf_order", "lt_leaf_order", "semisort", "local_refine", "collect_reduce",
     "DEPTH_LIMIT",
 ]
 
@@ -301,6 +301,40 @@ def semisort(keys, values, P: OracleParams, mode: str = "eq", identity: bool = F
         raise ValueError("params bound to another n")
     S = [np.empty_like(A[0]), None if A[1] is None else np.empty_like(A[1])]
     tel = OracleTelemetry(scratch_allocations=1)
+    _drive(A, S, [(0, n, 1, 0, True, 0, None, 0)], P, mode, identity, tel)
+    return A[0], A[1], tel
+
+
+def local_refine(primary, scratch, offsets, live_in_primary: bool, P: OracleParams, mode: str = "eq",
+                 identity: bool = False, depth: int = 0):
+    """core.py:533-563: refine the light buckets of a node already
+    distributed into the live buffer; returns (primary keys, values, tel).
+    primary / scratch: (keys, values) arrays of the node's size."""
+    A = [np.array(primary[0], copy=True), None if primary[1] is None else np.array(primary[1], copy=True)]
+    S = [np.array(scratch[0], copy=True), None if scratch[1] is None else np.array(scratch[1], copy=True)]
+    tel = OracleTelemetry()
+    off = [int(x) for x in offsets]
+    total = off[-1]
+    if not live_in_primary and off[P.n_light] < total:      # heavy buckets are final
+        h0 = off[P.n_light]
+        A[0][h0:total] = S[0][h0:total]
+        if A[1] is not None:
+            A[1][h0:total] = S[1][h0:total]
+    smalls, bigs = [], []
+    for b in range(P.n_light):
+        lo, hi = off[b], off[b + 1]
+        if hi > lo:
+            (smalls if hi - lo < P.alpha else bigs).append((b, lo, hi))
+    work = [(lo, hi, 1, depth + 1, live_in_primary, mix64_pair_int(P.seed, b + 1), total, 0)
+            for b, lo, hi in reversed(bigs)]
+    _drive(A, S, work, P, mode, identity, tel, first_leaves=[(lo, hi) for _, lo, hi in smalls],
+           leaves_in_a=live_in_primary)
+    return A[0], A[1], tel
+
+
+def _drive(A, S, work, P, mode, identity, tel, first_leaves=(), leaves_in_a=True):
+    """The recursion (core.py:437-530) as an explicit work list over
+    (lo, hi, level, depth, in_a, path, parent_size, stalled) nodes."""
 
     def buf(in_a):
         return A if in_a else S
@@ -319,7 +353,10 @@ def semisort(keys, values, P: OracleParams, mode: str = "eq", identity: bool = F
         if not in_a:
             move(A, slice(lo, hi), S, slice(lo, hi))
 
-    work = [(0, n, 1, 0, True, 0, None, 0)]
+    if first_leaves:
+        tel.seen(1, len(first_leaves))
+        for lo, hi in first_leaves:
+            leaf(lo, hi, leaves_in_a)
     while work:
         lo, hi, level, depth, in_a, path, parent, stalled = work.pop()
         size = hi - lo
@@ -355,7 +392,6 @@ def semisort(keys, values, P: OracleParams, mode: str = "eq", identity: bool = F
         for b, c_lo, c_hi in reversed(bigs):
             work.append((c_lo, c_hi, level + 1, depth + 1, not in_a,
                          mix64_pair_int(path, b + 1), size, stalled))
-    return A[0], A[1], tel
 
 
 # --------------------------------------------------------------------------

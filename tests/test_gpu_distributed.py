@@ -232,7 +232,9 @@ def test_validate_shard_and_fingerprints(S):
     assert r[0] == 0 and r[2] == 0 and r[3] == 0 and r[1] == count_distinct(d.keys)
     assert r[4:7] == [int(x) for x in fp]
     bad = d.copy()
-    bad.keys[7] ^= 1
+    kb = bad.keys.cpu().numpy()
+    kb[7] ^= np.uint64(1)
+    bad.keys.copy_(torch.from_numpy(kb))
     assert check(bad)[0] >= 1
     sw = d.copy()
     k = sw.keys.cpu().numpy()
