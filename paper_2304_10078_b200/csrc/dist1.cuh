@@ -24,6 +24,8 @@
 // buckets hold one key; the copy-back fills it, k_copy_heavy_fill).
 #pragma once
 
+#include <type_traits>
+
 #include "dist.cuh"
 
 namespace ss {
@@ -32,8 +34,13 @@ template <typename K, typename V, int TILE, int NT, int STAGES>
 struct Dist1Cfg : DistCfg<K, V, TILE, NT, STAGES> {
   using Base = DistCfg<K, V, TILE, NT, STAGES>;
   static constexpr int kWarps = NT / 32;
-  // u16 counter pairs per warp row: ceil(nb / 2) rounded up to even (uint2 loads)
-  __host__ __device__ static uint32_t pair_stride(uint32_t stride) { return ((stride + 1) / 2 + 1) & ~1u; }
+  // counter pairs a thread owns in the per-bucket scan: 2 (uint2 rows) at
+  // 512 consumer threads, 4 (uint4 rows) at 256
+  static constexpr int kQP = NT >= 512 ? 2 : 4;
+  // u16 counter pairs per warp row: ceil(nb / 2) rounded up to kQP (vector loads)
+  __host__ __device__ static uint32_t pair_stride(uint32_t stride) {
+    return ((stride + 1) / 2 + kQP - 1) & ~static_cast<uint32_t>(kQP - 1);
+  }
   static size_t smem_bytes(uint32_t stride) {
     return STAGES * Base::kSet + static_cast<size_t>(TILE) * 4 + 2 * Base::up16(static_cast<size_t>(stride) * 4) +
            static_cast<size_t>(kWarps) * pair_stride(stride) * 4 + 64;
@@ -48,8 +55,9 @@ struct Dist1Cfg : DistCfg<K, V, TILE, NT, STAGES> {
 // node's heavy region, so a node's heavy values lie contiguous inside its
 // heavy region's own words [2 hbase, hbase + h1) (the copy-back streams them;
 // keys are filled there).  Both need V == K.
-template <typename K, typename V, int TILE, int NT, int STAGES, bool SA = false, bool DA = false>
-__global__ void __launch_bounds__(NT + 32, 1)   // 17 warps: one sub-partition holds 5 -> <= 96 registers
+// MINB: CTAs per SM (2 with NT = 256: two independent consumer groups per SM)
+template <typename K, typename V, int TILE, int NT, int STAGES, bool SA = false, bool DA = false, int MINB = 1>
+__global__ void __launch_bounds__(NT + 32, MINB)   // 17 warps: one sub-partition holds 5 -> <= 96 registers
 
 k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t* __restrict__ ids, uint64_t n_src,
               K* __restrict__ dk, V* __restrict__ dv, const Work* __restrict__ work, uint32_t n_work,
@@ -182,48 +190,62 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
     //    Thread t owns pairs 2t, 2t+1 (one uint2 per warp row);
     //    thread-contiguous pairs keep the CTA scan in bucket order.
     uint32_t n_valid;
-    if (npairs <= 2 * NT) {
-      const uint32_t j0 = 2 * threadIdx.x;
+    constexpr int QP = Cfg::kQP;
+    using QV = std::conditional_t<QP == 2, uint2, uint4>;
+    if (npairs <= QP * NT) {
+      // thread t owns pairs QP t .. QP t + QP - 1 (one vector per warp row);
+      // thread-contiguous pairs keep the CTA scan in bucket order
+      const uint32_t j0 = QP * threadIdx.x;
       const bool own = j0 < npairs;
-      uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+      uint32_t lo[QP], hi[QP];
+#pragma unroll
+      for (int q = 0; q < QP; ++q) lo[q] = hi[q] = 0;
 #pragma unroll
       for (int v = 0; v < NW; ++v) {
-        const uint2 c = own ? *reinterpret_cast<const uint2*>(cntw + v * pstride + j0) : make_uint2(0, 0);
-        l0 += c.x & 0xFFFFu;
-        h0 += c.x >> 16;
-        l1 += c.y & 0xFFFFu;
-        h1 += c.y >> 16;
+        QV c{};
+        if (own) c = *reinterpret_cast<const QV*>(cntw + v * pstride + j0);
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(&c);
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+          lo[q] += cw[q] & 0xFFFFu;
+          hi[q] += cw[q] >> 16;
+        }
       }
+      uint32_t mine_tot = 0;
+#pragma unroll
+      for (int q = 0; q < QP; ++q) mine_tot += lo[q] + hi[q];
       unsigned long long total64;
-      const uint32_t s0 = static_cast<uint32_t>(cscan_u64<NW>(l0 + h0 + l1 + h1, red64, total64));
+      uint32_t a = static_cast<uint32_t>(cscan_u64<NW>(mine_tot, red64, total64));
       n_valid = static_cast<uint32_t>(total64);
       if (own) {
-        // bucket starts: 2j0, 2j0+1, 2j0+2, 2j0+3
-        uint32_t a0 = s0, a1 = s0 + l0, a2 = s0 + l0 + h0, a3 = s0 + l0 + h0 + l1;
-        const uint32_t b0 = 2 * j0;
-        wbase[b0] = cursor[b0] - a0;   // modular: cursor + (s - start) below
-        cursor[b0] += l0;
-        if (b0 + 1 < nb) {
-          wbase[b0 + 1] = cursor[b0 + 1] - a1;
-          cursor[b0 + 1] += h0;
-        }
-        if (b0 + 2 < nb) {
-          wbase[b0 + 2] = cursor[b0 + 2] - a2;
-          cursor[b0 + 2] += l1;
-        }
-        if (b0 + 3 < nb) {
-          wbase[b0 + 3] = cursor[b0 + 3] - a3;
-          cursor[b0 + 3] += h1;
+        uint32_t st[QP];   // packed tile starts of each owned pair (low | high << 16)
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+          const uint32_t b0 = 2 * (j0 + q);
+          const uint32_t alo = a, ahi = a + lo[q];
+          a = ahi + hi[q];
+          st[q] = alo | (ahi << 16);
+          if (b0 < nb) {   // modular: cursor + (s - start) below
+            wbase[b0] = cursor[b0] - alo;
+            cursor[b0] += lo[q];
+          }
+          if (b0 + 1 < nb) {
+            wbase[b0 + 1] = cursor[b0 + 1] - ahi;
+            cursor[b0 + 1] += hi[q];
+          }
         }
 #pragma unroll
         for (int v = 0; v < NW; ++v) {   // tile position of warp v's first record per bucket
-          uint2* cp = reinterpret_cast<uint2*>(cntw + v * pstride + j0);
-          const uint2 c = *cp;
-          *cp = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
-          a0 += c.x & 0xFFFFu;
-          a1 += c.x >> 16;
-          a2 += c.y & 0xFFFFu;
-          a3 += c.y >> 16;
+          QV* cp = reinterpret_cast<QV*>(cntw + v * pstride + j0);
+          QV c = *cp, o;
+          const uint32_t* cw = reinterpret_cast<const uint32_t*>(&c);
+          uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+          for (int q = 0; q < QP; ++q) {
+            ow[q] = st[q];
+            st[q] += cw[q];   // both halves advance; no carry (positions < 2^16)
+          }
+          *cp = o;
         }
       }
     } else {   // many buckets: contiguous chunks of pairs, counters re-read
@@ -281,11 +303,11 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
     mark(4);
 
     // D. sorted write-out (contiguous per-bucket runs); re-zero counters
-    if (npairs <= 2 * NT) {
-      const uint32_t j0 = 2 * threadIdx.x;
+    if (npairs <= QP * NT) {
+      const uint32_t j0 = QP * threadIdx.x;
       if (j0 < npairs)
 #pragma unroll
-        for (int v = 0; v < NW; ++v) *reinterpret_cast<uint2*>(cntw + v * pstride + j0) = make_uint2(0, 0);
+        for (int v = 0; v < NW; ++v) *reinterpret_cast<QV*>(cntw + v * pstride + j0) = QV{};
     } else {
       for (uint32_t j = threadIdx.x; j < npairs; j += NT)
 #pragma unroll

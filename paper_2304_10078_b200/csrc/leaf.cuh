@@ -104,13 +104,13 @@ __device__ __forceinline__ uint32_t warp_rank_item(bool valid, uint32_t key, uin
 // cursors cur; invalid positions (valid_of[p] == 0 when given) are skipped.
 // out may alias key_of.
 __device__ __forceinline__ void warp_walk(const uint32_t* key_of, const uint32_t* valid_of, uint32_t L,
-                                          uint32_t* mask, uint32_t* cur, uint32_t* out) {
+                                          uint32_t* mask, uint32_t* cur, uint32_t* out, bool hw = false) {
   const uint32_t lane = lane_id(), lt = lanemask_lt();
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t p = base + lane;
     const bool valid = p < L && (valid_of == nullptr || valid_of[p] != 0);
     const uint32_t k = valid ? key_of[p] : 0u;
-    const uint32_t r = warp_rank_item(valid, k, mask, cur, lane, lt);
+    const uint32_t r = warp_rank_item(valid, k, mask, cur, lane, lt, hw);
     if (valid) out[p] = r;
   }
 }
@@ -194,10 +194,43 @@ __device__ void leaf_eq(const K* rk, const V* rv, K* ok, V* ov, uint32_t m, bool
                         LeafArrays a, uint32_t* red, bool hw = false) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   const uint32_t cap = leaf_cap(m);
-  (void)hw;   // the CTA walk is one warp: its atomicOr ranks are not the bottleneck
   const bool one_cell = leaf_dedup(rk, m, cap, identity, a);
-  leaf_scan(a.cnt, m, red);
-  if (warp_id() == 0) warp_walk(a.pos, nullptr, m, a.mask, a.cnt, a.pos);   // pass 1
+  if (hw) {
+    // Pass 1 with lane-ordered atomics (probe.cuh), walking only records of
+    // groups with more than one record: a singleton group's record goes to
+    // its group start directly (all-distinct leaves -- uniform keys --
+    // skip the serial walk entirely).  Flags in mask[0, m) and arr (the
+    // non-hw walk's peer masks are not used), the list of walked records in
+    // T (free after the dedup).
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint32_t multi = a.cnt[a.pos[i]] > 1 ? 1u : 0u;
+      a.mask[i] = multi;
+      a.arr[i] = multi;
+    }
+    __syncthreads();
+    leaf_scan(a.cnt, m, red);   // group starts by first index
+    leaf_scan(a.arr, m, red);   // list positions
+    const uint32_t L = a.arr[m - 1] + a.mask[m - 1];
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      if (a.mask[i]) a.T[a.arr[i]] = i;
+      else a.pos[i] = a.cnt[a.pos[i]];
+    }
+    __syncthreads();
+    if (warp_id() == 0) {
+      const uint32_t lane = lane_id();
+      for (uint32_t b = 0; b < L; b += 32) {   // in index order: ranks inside each group
+        const uint32_t q = b + lane;
+        const uint32_t i = q < L ? a.T[q] : 0u;
+        const uint32_t f = q < L ? a.pos[i] : 0u;
+        const uint32_t r = q < L ? atomicAdd(&a.cnt[f], 1u) : 0u;
+        __syncwarp();
+        if (q < L) a.pos[i] = r;
+      }
+    }
+  } else {
+    leaf_scan(a.cnt, m, red);
+    if (warp_id() == 0) warp_walk(a.pos, nullptr, m, a.mask, a.cnt, a.pos);   // pass 1
+  }
   __syncthreads();
   if (!one_cell) {   // pass 2
     for (uint32_t c = threadIdx.x; c < cap; c += blockDim.x) a.T[c] = 0;
@@ -209,7 +242,7 @@ __device__ void leaf_eq(const K* rk, const V* rv, K* ok, V* ov, uint32_t m, bool
     }
     __syncthreads();
     leaf_scan(a.T, cap, red);
-    if (warp_id() == 0) warp_walk(a.arr, nullptr, m, a.mask, a.T, a.arr);
+    if (warp_id() == 0) warp_walk(a.arr, nullptr, m, a.mask, a.T, a.arr, hw);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) a.pos[i] = a.arr[a.pos[i]];
   }
