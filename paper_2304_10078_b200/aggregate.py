@@ -90,6 +90,8 @@ class KeyedResult:
                 self._pairs = []
             else:
                 ks = self.key_tensor.cpu().numpy().tolist()
+                if self.key_tensor.dim() == 2:   # 128-bit keys: (lo, hi) tuples like the reference's canonical
+                    ks = [tuple(k) for k in ks]
                 ag = self.agg_tensor.cpu().numpy().tolist()
                 self._pairs = list(zip(ks, ag))
         return self._pairs
@@ -145,9 +147,11 @@ def _device_kind(spec: ReduceSpec) -> int:
 def collect_reduce(data: RecordArray, adapter: KeyAdapter, spec: ReduceSpec, params: TuningParams | None = None,
                    *, workers: int | None = None, telemetry: Telemetry | None = None) -> KeyedResult:
     """Per-key count / wrapping-sum of ``data`` (aggregate.py:267-290)."""
-    ident = device_identity_flag(adapter)
+    ident = device_identity_flag(adapter, allow_u128=True)
     kind = _device_kind(spec)
-    kb, vb = _layout(data)
+    kb, vb = _layout(data, allow_u128=True)
+    if (kb == 16) != (data.key_kind == "u128") or (kb == 16) != (adapter.key_kind == "u128"):
+        raise ContractError(f"{type(adapter).__name__} does not match {data.key_kind} keys")
     n = len(data)
     params = _check_params(params, n)
     if kind == _lib.SS_AGG_SUM64 and data.values is None and n:
@@ -168,7 +172,7 @@ def collect_reduce(data: RecordArray, adapter: KeyAdapter, spec: ReduceSpec, par
                                      ws.data_ptr(), ws.numel(), C.byref(count), C.byref(ct), _stream(dev)))
     tel._absorb(ct)
     m = count.value
-    keys = torch.empty(m, dtype=data.keys.dtype, device=dev)
+    keys = torch.empty((m, 2) if kb == 16 else (m,), dtype=data.keys.dtype, device=dev)
     aggs = torch.empty(m, dtype=torch.uint64, device=dev)
     if m:
         _lib.check(lib.ss_result_copy(ws.data_ptr(), n, kb, vbytes, C.byref(pc), keys.data_ptr(), aggs.data_ptr(),

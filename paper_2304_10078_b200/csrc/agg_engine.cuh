@@ -44,11 +44,11 @@ namespace ss {
 template <typename K, typename V, bool SUM>
 __global__ void __launch_bounds__(kCountThreads)
 k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restrict__ work, uint32_t n_work,
-            const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, KeyBuckets bf,
+            const Node* __restrict__ nodes, uint32_t* __restrict__ C, uint32_t stride, KeyBucketsT<KeyStore<K>> bf,
             unsigned long long* __restrict__ HS, uint32_t hs_stride, uint16_t* __restrict__ ids_out,
             uint32_t ss = 1) {   // ss 2: (key, value) pair records
   extern __shared__ __align__(16) uint32_t cnt[];
-  __shared__ HeavySmem tab;
+  __shared__ HeavySmemT<KeyStore<K>> tab;
   // heavy partial sums as native 32-bit atomics: low half, carries out of
   // it, high half (a 64-bit shared atomicAdd is a CAS spin loop on sm_100)
   __shared__ uint32_t hlo[kMaxHeavyDevice], hhi[kMaxHeavyDevice], hcy[kMaxHeavyDevice];
@@ -155,7 +155,7 @@ k_count_agg(const K* __restrict__ src, const V* __restrict__ sv, Work* __restric
 template <typename K, bool SUM>
 __global__ void k_heavy_fold(const Node* __restrict__ nodes, uint32_t n_nodes, const uint32_t* __restrict__ C,
                              uint32_t stride, uint32_t n_light, const unsigned long long* __restrict__ HS,
-                             uint32_t hs_stride, const uint64_t* __restrict__ heavy, uint32_t mh,
+                             uint32_t hs_stride, const KeyStore<K>* __restrict__ heavy, uint32_t mh,
                              K* __restrict__ hk, uint64_t* __restrict__ ha) {
   for (uint32_t j = blockIdx.x; j < n_nodes; j += gridDim.x) {
     const Node nd = nodes[j];
@@ -379,7 +379,7 @@ struct AggEngine {
   uint64_t* st_a = nullptr;
   Node* d_nodes = nullptr;
   Node* d_next = nullptr;
-  uint64_t* d_heavy = nullptr;
+  KeyStore<K>* d_heavy = nullptr;
   Work* d_work = nullptr;
   uint32_t* d_grp_node = nullptr;
   uint32_t* d_C = nullptr;
@@ -437,7 +437,7 @@ struct AggEngine {
     st_a = a.take<uint64_t>(n);
     d_nodes = a.take<Node>(max_nodes);
     d_next = a.take<Node>(max_nodes);
-    d_heavy = a.take<uint64_t>(max_nodes * mh);
+    d_heavy = a.take<KeyStore<K>>(max_nodes * mh);
     d_work = a.take<Work>(max_rows);
     d_grp_node = a.take<uint32_t>(max_grps);
     d_C = a.take<uint32_t>(max_rows * stride);
@@ -448,7 +448,7 @@ struct AggEngine {
     d_misc = a.take<uint64_t>(8);
     d_leaf_s = a.take<Leaf>(max_leaves);
     d_leaf_g = a.take<Leaf>(max_leaves);
-    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * sample_scratch_words(s_cap, 8));
+    d_samp = a.take<uint64_t>(static_cast<uint64_t>(sample_grid) * sample_scratch_words(s_cap, sizeof(KeyStore<K>)));
     d_leafscr = a.take<uint32_t>(static_cast<uint64_t>(leafg_grid) * leafg_words);
     d_HS = a.take<unsigned long long>(max_rows * mh);
     d_ntot = a.take<uint64_t>(max_nodes);
@@ -541,6 +541,10 @@ struct AggEngine {
   // nodes that need the regular level path (children >= alpha, or more
   // distinct keys than the shared-memory table holds).
   std::vector<Node> fold_nodes(Tracker& tr, std::vector<Node>& cur, int lvl) {
+    if constexpr (sizeof(K) > 8) return cur;   // 128-bit keys: the level path (no 16-byte fold table)
+    else return fold_nodes_impl(tr, cur, lvl);
+  }
+  std::vector<Node> fold_nodes_impl(Tracker& tr, std::vector<Node>& cur, int lvl) {
     const K* sk = B_k[lvl & 1];
     const V* sv = B_v[lvl & 1];
     std::vector<Node> rest, fold;
@@ -676,7 +680,7 @@ struct AggEngine {
     check_launch();
     tr.launched();
 
-    KeyBuckets bf{};
+    KeyBucketsT<KeyStore<K>> bf{};
     bf.heavy = d_heavy;
     bf.max_heavy = mh;
     bf.n_light = P.light_buckets;

@@ -35,8 +35,8 @@ void dispatch_kv(uint32_t kb, uint32_t vb, F&& f) {
   }
 }
 
-// dispatch_kv plus 128-bit keys (records.py:8-10): the semisort entry points
-// only; aggregation and the phase-level API stay 32/64-bit.
+// dispatch_kv plus 128-bit keys (records.py:8-10): the semisort and
+// aggregation entry points; the phase-level API stays 32/64-bit.
 template <typename F>
 void dispatch_sort(uint32_t kb, uint32_t vb, F&& f) {
   check_widths(kb, vb, true);
@@ -336,7 +336,7 @@ uint64_t ss_aggregate_workspace_bytes(uint64_t n, uint32_t key_bytes, uint32_t v
   uint64_t out = 0;
   int rc = guarded([&] {
     Params P = to_params(params, n, false);
-    dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
+    dispatch_sort(key_bytes, value_bytes, [&]<typename K, typename V>() {
       AggEngine<K, V> e{};
       e.n = n;
       e.P = P;
@@ -358,7 +358,7 @@ int ss_collect_reduce(const void* keys, const void* values, uint64_t n, uint32_t
       throw Fail(SS_ERR_CONFIG, "summing64 needs a value column");
     if (!out_count) throw Fail(SS_ERR_CONFIG, "out_count must not be NULL");
     reset_tel(telemetry);
-    dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
+    dispatch_sort(key_bytes, value_bytes, [&]<typename K, typename V>() {
       AggEngine<K, V> e{};
       e.in_k = static_cast<const K*>(keys);
       e.in_v = static_cast<const V*>(values);
@@ -389,7 +389,7 @@ int ss_result_copy(const void* workspace, uint64_t n, uint32_t key_bytes, uint32
                    const ss_params* params, void* out_keys, void* out_aggs, uint64_t count, void* stream) {
   return guarded([&] {
     Params P = to_params(params, n, false);
-    dispatch_kv(key_bytes, value_bytes, [&]<typename K, typename V>() {
+    dispatch_sort(key_bytes, value_bytes, [&]<typename K, typename V>() {
       AggEngine<K, V> e{};
       e.n = n;
       e.P = P;

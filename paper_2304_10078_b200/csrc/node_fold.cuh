@@ -21,12 +21,15 @@
 // takes the regular level path (the table is discarded, nothing was
 // written; u32 counting also falls back when a 16-bit count wrapped).
 //
-// Table: buckets of 16 bytes (4 u32 or 2 u64 slots), one shared load each;
+// Table (u32 counting, c4: ~9.8K keys per node at load 0.3): buckets of 16
+// bytes (4 slots), one shared load each;
 // a key's home bucket is a multiplicative fold of the raw key (independent
 // of the hash bits the node's ancestors bucketed on); slots fill a bucket
 // left to right, the next bucket takes the overflow, the ones after it
 // when both are full (fold_probe2).  Per record: one vector load (two when
-// the home bucket is full), compares, one shared atomicAdd (+1-2 for sums).
+// the home bucket is full), compares, one shared atomicAdd.  Other key /
+// aggregate types (few keys per node, e.g. c3's ~120): single-slot linear
+// probing, one 8-byte load per record, + 1-2 atomics for sums.
 // The kernel is bound by shared-memory wavefronts (bank conflicts of the
 // random bucket loads and counter atomics), not by HBM.
 //
@@ -191,6 +194,10 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
   const volatile uint32_t* vfail = &s_fail;
 
   auto home = [](TK k) { return static_cast<uint32_t>((static_cast<uint64_t>(k) * kGamma) >> (64 - Sh::kLog2B)); };
+  auto probe_start = [](TK k) {   // first slot of the single-slot probe (!C16)
+    const uint32_t x = static_cast<uint32_t>(k) ^ static_cast<uint32_t>(static_cast<uint64_t>(k) >> 32);
+    return (x * 0x9E3779B1u) >> (32 - Sh::kLog2T);
+  };
   auto add_sum = [&](uint32_t* lo, uint32_t* hi, uint64_t v) {
     const uint32_t l = static_cast<uint32_t>(v), h = static_cast<uint32_t>(v >> 32);
     const uint32_t old = atomicAdd(lo, l);
@@ -203,6 +210,34 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
     if (k == kEmpty) {
       atomicAdd(&e_cnt, 1u);
       if constexpr (SUM) add_sum(&e_lo, &e_hi, v);
+      return;
+    }
+    if constexpr (!C16) {
+      // few distinct keys per node (c3: ~120): single-slot linear probing
+      // from a multiplicative hash of the raw key -- one 8-byte shared load
+      // per record instead of a 16-byte bucket scan (c3 fold 3.79 -> 3.28
+      // ms).  At c4's load 0.3 the probe chains diverged (max over a warp
+      // ~3 probes): u32 counting keeps the bucket scan below.
+      uint32_t slot = probe_start(k);
+      for (uint32_t n = 0;; ++n) {
+        TK t = tk[slot];
+        if (t == k) break;
+        if (t == kEmpty) {
+          t = atomicCAS(const_cast<TK*>(tk + slot), kEmpty, k);
+          if (t == kEmpty) {
+            if (atomicAdd(&s_used, 1u) >= Sh::kLimit) s_fail = 1;
+            break;
+          }
+          if (t == k) break;
+        }
+        if (n + 1 >= T) {   // table full
+          s_fail = 1;
+          return;
+        }
+        slot = (slot + 1) & (T - 1);
+      }
+      c_red(cnt, slot);
+      if constexpr (SUM) add_sum(&slo[slot], &shi[slot], v);
       return;
     }
     // the home bucket, then the next one only when it is full (a second

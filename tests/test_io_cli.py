@@ -202,8 +202,6 @@ def test_cli_errors(S, tmp_path):
 @pytest.mark.parametrize("algo", ["eq", "lt", "int-eq", "int-lt", "histogram", "collect-reduce"])
 @pytest.mark.parametrize("bits", [32, 64, 128])
 def test_cli_bench_rows(S, algo, bits):
-    if bits == 128 and algo in ("histogram", "collect-reduce"):
-        pytest.skip("aggregation stays 32/64-bit on the GPU path")
     dist, param = ("zipfian", "1.2") if bits != 32 else ("uniform", "5000")
     rc, out, err = _cli(["bench", "--algo", algo, "--dist", dist, "--param", param, "--n", "200000",
                          "--key-bits", str(bits), "--reps", "2", "--verify"])

@@ -142,5 +142,89 @@ def test_u128_errors(S):
         S.semisort(S.RecordArray(k), S.UIntKeyAdapter(), "eq")
     with pytest.raises(S.ContractError):
         S.semisort(S.RecordArray(np.array([1, 2], np.uint64)), S.UInt128KeyAdapter(), "eq")
-    with pytest.raises(S.ContractError):            # aggregation stays 32/64-bit
-        S.histogram(S.RecordArray(k), S.UInt128KeyAdapter())
+    with pytest.raises(S.ContractError):            # aggregation: adapter / key kind mismatch
+        S.histogram(S.RecordArray(k), S.UIntKeyAdapter())
+    with pytest.raises(S.ContractError):
+        S.histogram(S.RecordArray(np.array([1, 2], np.uint64)), S.UInt128KeyAdapter())
+
+
+# ---- collect_reduce / histogram over 128-bit keys (aggregate.py:267-299) -----
+
+GA = np.load(os.path.join(HERE, "golden", "golden_u128_agg.npz"))
+AGG_TAGS = [str(t) for t in GA["tags"]]
+AGG_META = __import__("json").loads(str(GA["meta"]))
+
+
+def _agg_split(tag):
+    case, kind, ident = tag.rsplit("_", 2)
+    return case, kind, ident == "1"
+
+
+def _multiset(k, a):
+    k = np.asarray(k, dtype=np.uint64).reshape(-1, 2)
+    order = np.lexsort((k[:, 0], k[:, 1]))
+    return k[order], np.asarray(a, dtype=np.uint64)[order]
+
+
+@pytest.mark.parametrize("tag", AGG_TAGS)
+def test_u128_aggregate_fixture_semantics(tag):
+    """The reference's pairs are one (key, count | wrapping sum) per distinct
+    128-bit key (numpy restatement: unique rows + bincount / add.at)."""
+    case, kind, _ = _agg_split(tag)
+    keys = G[f"{case}_keys"]
+    uniq, inv = np.unique(keys, axis=0, return_inverse=True) if len(keys) else (np.zeros((0, 2), np.uint64), None)
+    if kind == "count":
+        agg = np.bincount(inv.ravel(), minlength=len(uniq)).astype(np.uint64) if len(keys) else np.zeros(0, np.uint64)
+    else:
+        agg = np.zeros(len(uniq), dtype=np.uint64)
+        if len(keys):
+            np.add.at(agg, inv.ravel(), GA[f"{case}_vals"])
+    rk, ra = _multiset(GA[f"{tag}_k"], GA[f"{tag}_a"])
+    ek, ea = _multiset(uniq, agg)
+    assert np.array_equal(rk, ek) and np.array_equal(ra, ea)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", AGG_TAGS)
+def test_u128_aggregate_gpu_matches_reference(S, tag):
+    case, kind, ident = _agg_split(tag)
+    keys = G[f"{case}_keys"]
+    n = len(keys)
+    params = S.TuningParams.for_input(n, **_kw(case))
+    adp = S.UInt128KeyAdapter(identity=ident)
+    tel = S.Telemetry()
+    if kind == "count":
+        res = S.histogram(S.RecordArray(keys), adp, params, telemetry=tel)
+    else:
+        res = S.collect_reduce(S.RecordArray(keys, GA[f"{case}_vals"]), adp, S.ReduceSpec.summing64(), params,
+                               telemetry=tel)
+    k, a = res.to_numpy()
+    rk, ra = _multiset(GA[f"{tag}_k"], GA[f"{tag}_a"])
+    gk, ga = _multiset(k, a)
+    assert np.array_equal(gk, rk) and np.array_equal(ga, ra)
+    ref = AGG_META[tag]
+    assert (tel.max_depth, tel.nodes, tel.scratch_moves, tel.bucket_assignments) == \
+        (ref["max_depth"], ref["nodes"], ref["scratch_moves"], ref["bucket_assignments"])
+    assert {str(k): v for k, v in tel.matrix_cells_by_level.items()} == ref["matrix_cells_by_level"]
+    if n:
+        assert res.pairs and isinstance(res.pairs[0][0], tuple)   # (lo, hi) like the reference
+
+
+@pytest.mark.gpu
+def test_u128_aggregate_1m_vs_numpy(S):
+    rng = np.random.default_rng(29)
+    n = 1 << 20
+    keys = _u128_keys(rng, n, "zipf")
+    vals = rng.integers(0, 2**63, n).astype(np.uint64)
+    uniq, inv = np.unique(keys, axis=0, return_inverse=True)
+    cnt = np.bincount(inv.ravel(), minlength=len(uniq)).astype(np.uint64)
+    sm = np.zeros(len(uniq), dtype=np.uint64)
+    np.add.at(sm, inv.ravel(), vals)
+    for kind, want in (("count", cnt), ("sum64", sm)):
+        if kind == "count":
+            res = S.histogram(S.RecordArray(keys), S.UInt128KeyAdapter())
+        else:
+            res = S.collect_reduce(S.RecordArray(keys, vals), S.UInt128KeyAdapter(), S.ReduceSpec.summing64())
+        gk, ga = _multiset(*res.to_numpy())
+        ek, ea = _multiset(uniq, want)
+        assert np.array_equal(gk, ek) and np.array_equal(ga, ea)
