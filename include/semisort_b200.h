@@ -318,6 +318,27 @@ int ss_records_unpack(const void* rows, uint64_t n, uint32_t key_bytes, uint32_t
 int ss_records_pack(const void* keys, const void* values, uint64_t n, uint32_t key_bytes, uint32_t value_bytes,
                     void* rows, void* stream);
 
+/* ---- byte-view keys (adapters.py:200-275, hashing.py:56-106, ngrams.py) --
+ * Keys are (offset, length) u64 rows (views, device) into a device byte
+ * arena of arena_len bytes.  The Python layer (bytes_keys.py) turns them into
+ * 128-bit identity keys (lo = content hash, hi = length for semisort= /
+ * aggregation, = exact lexicographic content rank for semisort<) and runs
+ * ss_semisort / ss_collect_reduce on those; these calls supply the pieces.
+ * counter: one u64 of device scratch.
+ *
+ * ss_bytes_hash: out_hash[i] = mix64(poly(bytes) ^ mix64(len)), poly the
+ *   wrapping polynomial with multiplier 0x100000001B3 (hashing.py:56-66 /
+ *   BytePrefixHasher.hash_views :98-106).  SS_ERR_CONFIG when a view leaves
+ *   the arena.
+ * ss_bytes_chunk: out[i] = bytes [7c, 7c+7) of view i as 9-bit digits
+ *   (byte + 1, 0 past the end), int64: lexicographic order chunk by chunk.
+ * ss_bytes_equal: *out_mismatches = #{i : content(a[i]) != content(b[i])}. */
+int ss_bytes_hash(const void* arena, uint64_t arena_len, const void* views, uint64_t n, void* out_hash,
+                  void* counter, void* stream);
+int ss_bytes_chunk(const void* arena, const void* views, uint64_t n, uint64_t chunk, void* out, void* stream);
+int ss_bytes_equal(const void* arena, const void* views_a, const void* views_b, uint64_t n, void* counter,
+                   uint64_t* out_mismatches, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,3 +15,4 @@ from .semisort_oracle import *  # noqa: F401,F403
 from .checkers import *  # noqa: F401,F403
 from .graphs_oracle import csr_from_edges, transpose as graph_transpose  # noqa: F401
 from .records_oracle import dump_bytes, pack_rows, parse_dump  # noqa: F401
+from .bytes_oracle import hash_bytes, semisort_bytes  # noqa: F401

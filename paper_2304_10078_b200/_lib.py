@@ -77,6 +77,9 @@ _SIGS = {
                                 C.POINTER(SSTelemetry), vp]),
     "ss_records_unpack": (i32, [vp, u64, u32, u32, vp, vp, vp]),
     "ss_records_pack": (i32, [vp, vp, u64, u32, u32, vp, vp]),
+    "ss_bytes_hash": (i32, [vp, u64, vp, u64, vp, vp, vp]),
+    "ss_bytes_chunk": (i32, [vp, vp, u64, u64, vp, vp]),
+    "ss_bytes_equal": (i32, [vp, vp, vp, u64, vp, C.POINTER(C.c_uint64), vp]),
     "ss_partition_pairs": (i32, [vp, vp, u64, u32, u32, vp, C.POINTER(u64), vp, u64, vp]),
     "ss_partition_pairs_workspace_bytes": (u64, [u64, u32]),
     "ss_semisort_pairs": (i32, [vp, u64, u32, i32, i32, C.POINTER(SSParams), vp, vp, u64,

@@ -2,11 +2,12 @@
 
 The GPU path implements the fixed-width integer adapters: hash =
 mix64(u64(key)) or the identity (adapters.py:112-119), equality on the key
-bits, stable order by key value; and, for semisort only, the 128-bit adapter
-(hash mix64(mix64(hi) ^ lo) or lo, order (hi, lo); adapters.py:147-198).  Any
+bits, stable order by key value; the 128-bit adapter (hash mix64(mix64(hi) ^
+lo) or lo, order (hi, lo); adapters.py:147-198); and byte-view keys
+(content hash, content equality and order; adapters.py:200-275).  Any
 adapter whose hash or equality is arbitrary Python (a subclass overriding
-them, byte-view keys) cannot run on the device and is rejected with
-ContractError instead of being silently executed on the CPU.
+them) cannot run on the device and is rejected with ContractError instead of
+being silently executed on the CPU.
 """
 
 from __future__ import annotations
@@ -53,8 +54,8 @@ class UIntKeyAdapter(KeyAdapter):
 class UInt128KeyAdapter(KeyAdapter):
     """128-bit keys as (lo, hi) word pairs (adapters.py:147-198).
 
-    semisort runs them on the device; the aggregation and phase-level entry
-    points stay 32/64-bit and reject them with ContractError.
+    semisort, collect_reduce and histogram run them on the device; the
+    phase-level entry points stay 32/64-bit and reject them with ContractError.
     """
 
     key_kind = "u128"
@@ -69,13 +70,34 @@ class UInt128KeyAdapter(KeyAdapter):
         return lo if self.identity_mode else _mix64(_mix64(hi & U64_MASK) ^ lo)
 
 
+_POLY_MULT = 0x100000001B3   # hashing.py:19 (the FNV-1a prime)
+
+
+def hash_bytes(data: bytes) -> int:
+    """Host scalar form of the content hash (hashing.py:56-66): mix64 of the
+    wrapping polynomial over the bytes xor mix64(len).  The device computes
+    the same (ss_bytes_hash)."""
+    acc = 0
+    for b in bytes(data):
+        acc = (acc * _POLY_MULT + b) & U64_MASK
+    return _mix64(acc ^ _mix64(len(data)))
+
+
 class BytesKeyAdapter(KeyAdapter):
-    """Byte-view keys: part of the reference API, not of the GPU hot path."""
+    """Byte-view keys over a shared arena (adapters.py:200-275): equality and
+    order compare the referenced bytes, the hash is the content polynomial
+    (offsets never matter).  On the GPU (bytes_keys.py) the views become
+    128-bit identity keys (content hash, length or exact content rank)."""
 
     key_kind = "bytes"
+    identity_mode = False
+    has_lt = True
 
     def __init__(self, arena=None):
         self.arena = arena
+
+    def hash_scalar(self, key) -> int:
+        return hash_bytes(key)
 
 
 def adapter_for(data, *, identity: bool = False) -> KeyAdapter:

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .adapters import KeyAdapter, device_identity_flag
+from .adapters import BytesKeyAdapter, KeyAdapter, UInt128KeyAdapter, device_identity_flag
 from .core import Telemetry, _check_params, _layout, _ptr, _stream, _workspace
 from .errors import ConfigurationError, ContractError
 from .params import TuningParams
@@ -76,12 +76,13 @@ class KeyedResult:
     materialised lazily from the tensors.
     """
 
-    __slots__ = ("_pairs", "key_tensor", "agg_tensor")
+    __slots__ = ("_pairs", "key_tensor", "agg_tensor", "arena")
 
-    def __init__(self, pairs: list | None = None, *, key_tensor=None, agg_tensor=None):
+    def __init__(self, pairs: list | None = None, *, key_tensor=None, agg_tensor=None, arena=None):
         self._pairs = pairs
         self.key_tensor = key_tensor
         self.agg_tensor = agg_tensor
+        self.arena = arena   # byte-view keys: key_tensor holds (offset, length) views into it
 
     @property
     def pairs(self) -> list:
@@ -90,7 +91,10 @@ class KeyedResult:
                 self._pairs = []
             else:
                 ks = self.key_tensor.cpu().numpy().tolist()
-                if self.key_tensor.dim() == 2:   # 128-bit keys: (lo, hi) tuples like the reference's canonical
+                if self.arena is not None:   # byte-view keys: the content bytes (adapters.py:216-218)
+                    buf = self.arena.cpu().numpy().tobytes()
+                    ks = [buf[o:o + n] for o, n in ks]
+                elif self.key_tensor.dim() == 2:   # 128-bit keys: (lo, hi) tuples like the reference's canonical
                     ks = [tuple(k) for k in ks]
                 ag = self.agg_tensor.cpu().numpy().tolist()
                 self._pairs = list(zip(ks, ag))
@@ -108,7 +112,7 @@ class KeyedResult:
         if not isinstance(other, KeyedResult):
             return False
         if self.key_tensor is not None and other.key_tensor is not None and self._pairs is None \
-                and other._pairs is None:
+                and other._pairs is None and self.arena is None and other.arena is None:
             return self.key_tensor.shape == other.key_tensor.shape and \
                 self.key_tensor.dtype == other.key_tensor.dtype and \
                 torch.equal(signed_view(self.key_tensor), signed_view(other.key_tensor.to(self.key_tensor.device))) \
@@ -147,6 +151,8 @@ def _device_kind(spec: ReduceSpec) -> int:
 def collect_reduce(data: RecordArray, adapter: KeyAdapter, spec: ReduceSpec, params: TuningParams | None = None,
                    *, workers: int | None = None, telemetry: Telemetry | None = None) -> KeyedResult:
     """Per-key count / wrapping-sum of ``data`` (aggregate.py:267-290)."""
+    if getattr(data, "key_kind", None) == "bytes" or isinstance(adapter, BytesKeyAdapter):
+        return _collect_reduce_bytes(data, adapter, spec, params, telemetry)
     ident = device_identity_flag(adapter, allow_u128=True)
     kind = _device_kind(spec)
     kb, vb = _layout(data, allow_u128=True)
@@ -178,6 +184,21 @@ def collect_reduce(data: RecordArray, adapter: KeyAdapter, spec: ReduceSpec, par
         _lib.check(lib.ss_result_copy(ws.data_ptr(), n, kb, vbytes, C.byref(pc), keys.data_ptr(), aggs.data_ptr(),
                                       m, _stream(dev)))
     return KeyedResult(key_tensor=keys, agg_tensor=aggs)
+
+
+def _collect_reduce_bytes(data, adapter, spec, params, telemetry) -> KeyedResult:
+    """Byte-view keys (adapters.py:200-275): aggregation of 128-bit identity
+    keys (content hash, length), then one representative view per distinct
+    content, byte-checked against every record of its group (bytes_keys.py).
+    Result keys are the content bytes, as the reference's canonical()."""
+    from . import bytes_keys
+    if not isinstance(adapter, BytesKeyAdapter) or getattr(data, "key_kind", None) != "bytes":
+        raise ContractError(f"{type(adapter).__name__} does not match {getattr(data, 'key_kind', None)} keys")
+    syn = bytes_keys.synthetic_keys(data, "eq")
+    res = collect_reduce(RecordArray(syn, data.values, "u128"), UInt128KeyAdapter(identity=True), spec, params,
+                         telemetry=telemetry)
+    views = bytes_keys.representatives(data, syn, res.key_tensor)
+    return KeyedResult(key_tensor=views, agg_tensor=res.agg_tensor, arena=data.arena)
 
 
 def histogram(data: RecordArray, adapter: KeyAdapter, params: TuningParams | None = None, *,

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .adapters import KeyAdapter, UIntKeyAdapter, device_identity_flag
+from .adapters import BytesKeyAdapter, KeyAdapter, UInt128KeyAdapter, UIntKeyAdapter, device_identity_flag
 from .errors import ConfigurationError, ContractError
 from .params import TuningParams
 from .records import RecordArray, as_device_column, signed_view
@@ -440,6 +440,8 @@ def semisort(data: RecordArray, adapter: KeyAdapter, mode: str = "eq", params: T
         raise ConfigurationError(f"mode must be 'eq' or 'lt', got {mode!r}")
     if mode == "lt" and not adapter.has_lt:
         raise ContractError("mode 'lt' requires an adapter with a less-than test")
+    if getattr(data, "key_kind", None) == "bytes" or isinstance(adapter, BytesKeyAdapter):
+        return _semisort_bytes(data, adapter, mode, params, telemetry)
     ident = device_identity_flag(adapter, allow_u128=True)
     kb, vb = _layout(data, allow_u128=True)
     if (data.key_kind == "u128") != (adapter.key_kind == "u128"):
@@ -458,6 +460,33 @@ def semisort(data: RecordArray, adapter: KeyAdapter, mode: str = "eq", params: T
                                       _lib.SS_MODE_LT if mode == "lt" else _lib.SS_MODE_EQ, ident, C.byref(pc),
                                       ws.data_ptr(), ws.numel(), C.byref(ct), _stream(dev)))
     tel._absorb(ct)
+    return data
+
+
+def _semisort_bytes(data, adapter, mode, params, telemetry):
+    """Byte-view keys (adapters.py:200-275): semisort of 128-bit identity keys
+    (content hash, length | content rank) carrying the record index, then the
+    caller's views and values are permuted in place (bytes_keys.py)."""
+    from . import bytes_keys
+    if not isinstance(adapter, BytesKeyAdapter) or getattr(data, "key_kind", None) != "bytes":
+        raise ContractError(f"{type(adapter).__name__} does not match {getattr(data, 'key_kind', None)} keys")
+    if type(adapter).hash_scalar is not BytesKeyAdapter.hash_scalar:
+        raise ContractError(f"{type(adapter).__name__}.hash_scalar is custom Python; the GPU path only runs the "
+                            "reference's content hash")
+    if data.values is not None and data.value_bytes not in (4, 8, 16):
+        raise ContractError(f"value rows of {data.value_bytes} bytes are not supported by the GPU path")
+    n = len(data)
+    params = _check_params(params, n)
+    syn = bytes_keys.synthetic_keys(data, mode)
+    idx = torch.arange(n, dtype=torch.int64, device=data.device).view(torch.uint64)
+    tmp = RecordArray(syn, idx, "u128")
+    semisort(tmp, UInt128KeyAdapter(identity=True), mode, params, telemetry=telemetry)
+    perm = tmp.values.view(torch.int64)
+    if mode == "eq":
+        bytes_keys.check_grouped(data, tmp.keys, perm)
+    data.keys.copy_(data.keys.view(torch.int64)[perm].view(torch.uint64))
+    if data.values is not None:
+        data.values.copy_(signed_view(data.values)[perm].view(data.values.dtype))
     return data
 
 

@@ -59,6 +59,17 @@ def as_device_column(a, dtype: torch.dtype | None = None, device=None) -> torch.
     return torch.from_numpy(arr).to(device or default_device())
 
 
+def as_byte_arena(a, device) -> torch.Tensor:
+    """A contiguous uint8 CUDA tensor for a byte arena (bytes / numpy / tensor)."""
+    if isinstance(a, torch.Tensor):
+        t = a if a.dtype == torch.uint8 else a.view(torch.uint8)
+        return t.to(device).contiguous()
+    if isinstance(a, (bytes, bytearray, memoryview)):
+        a = np.frombuffer(bytes(a), dtype=np.uint8)
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.uint8))
+    return torch.from_numpy(arr.copy()).to(device)
+
+
 class RecordArray:
     """Records (key, value) as device columns; mirrors records.py:34-132."""
 
@@ -66,7 +77,11 @@ class RecordArray:
 
     def __init__(self, keys, values=None, key_kind=None, arena=None):
         if key_kind == "bytes" or arena is not None:
-            raise InputFormatError("byte-view keys are not supported by the GPU path")
+            if key_kind not in (None, "bytes"):
+                raise ValueError(f"an arena goes with byte-view keys, not {key_kind!r}")
+            if arena is None:
+                raise ValueError("bytes keys require an arena")
+            key_kind = "bytes"
         if isinstance(keys, torch.Tensor):
             kt = keys
         else:
@@ -98,7 +113,9 @@ class RecordArray:
                 raise ValueError("values length must match keys length")
         self.keys = kt
         self.values = vt
-        self.arena = None
+        # byte-view keys: (offset, length) rows into a shared, caller-owned
+        # uint8 arena (records.py:11-13), kept on the device next to them
+        self.arena = None if arena is None else as_byte_arena(arena, kt.device)
         self.key_kind = key_kind
 
     # -- shape & views --------------------------------------------------------
@@ -111,7 +128,7 @@ class RecordArray:
 
     @property
     def key_bytes(self) -> int:
-        return self.keys.element_size() * (2 if self.key_kind == "u128" else 1)
+        return self.keys.element_size() * (2 if self.key_kind in ("u128", "bytes") else 1)
 
     @property
     def value_bytes(self) -> int:
@@ -127,13 +144,13 @@ class RecordArray:
         out = RecordArray.__new__(RecordArray)
         out.keys = self.keys[lo:hi]
         out.values = None if self.values is None else self.values[lo:hi]
-        out.arena = None
+        out.arena = self.arena
         out.key_kind = self.key_kind
         return out
 
     def _wrap(self, keys, values) -> "RecordArray":
         out = RecordArray.__new__(RecordArray)
-        out.keys, out.values, out.arena, out.key_kind = keys, values, None, self.key_kind
+        out.keys, out.values, out.arena, out.key_kind = keys, values, self.arena, self.key_kind
         return out
 
     def copy(self) -> "RecordArray":

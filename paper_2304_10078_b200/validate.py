@@ -81,6 +81,17 @@ def _flat_keys(k: np.ndarray) -> np.ndarray:
     return k if k.ndim == 1 else np.ascontiguousarray(k).view(np.dtype((np.void, 16))).ravel()
 
 
+def _content_ids(a: RecordArray, b: RecordArray):
+    """Dense ids of the views' contents (equal bytes -> equal id), both arrays."""
+    seen: dict[bytes, int] = {}
+
+    def ids(d):
+        buf = d.arena.cpu().numpy().tobytes()
+        return np.array([seen.setdefault(buf[o:o + n], len(seen)) for o, n in d.keys_host().tolist()],
+                        dtype=np.int64)
+    return ids(a), ids(b)
+
+
 def validate_semisort(input_data: RecordArray, output_data: RecordArray, adapter=None) -> ValidationReport:
     n = len(input_data)
     if len(output_data) != n:
@@ -90,7 +101,10 @@ def validate_semisort(input_data: RecordArray, output_data: RecordArray, adapter
     if input_data.key_kind in ("u32", "u64") and _is_index_column(input_data.values):
         return validate_indexed(input_data.keys, output_data.keys, output_data.values)
     # definition-level host check (checker only)
-    ki, ko = _flat_keys(input_data.keys_host()), _flat_keys(output_data.keys_host())
+    if input_data.key_kind == "bytes":   # byte-view keys compare by content (adapters.py:200-275)
+        ki, ko = _content_ids(input_data, output_data)
+    else:
+        ki, ko = _flat_keys(input_data.keys_host()), _flat_keys(output_data.keys_host())
     brk = np.ones(n, dtype=bool)
     brk[1:] = ko[1:] != ko[:-1]
     contiguous = len(np.unique(ko[brk])) == int(brk.sum())
