@@ -137,8 +137,8 @@ __device__ inline void leaf_scan(uint32_t* a, uint32_t L, uint32_t* red) {
 // ks: element stride of rk (2 when the records are (key, value) pairs).
 template <typename K>
 __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity, LeafArrays a, bool count = true,
-                           uint32_t ks = 1) {
-  __shared__ uint32_t s_cmin, s_cmax;
+                           uint32_t ks = 1, uint32_t* groups = nullptr) {   // groups: distinct keys (shared)
+  __shared__ uint32_t s_cmin, s_cmax, s_groups;
   const uint32_t cmask = cap - 1;
   for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
     a.T[s] = kEmpty32;
@@ -148,9 +148,10 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
   if (threadIdx.x == 0) {
     s_cmin = 0xFFFFFFFFu;
     s_cmax = 0;
+    s_groups = 0;
   }
   __syncthreads();
-  uint32_t cmin = 0xFFFFFFFFu, cmax = 0;
+  uint32_t cmin = 0xFFFFFFFFu, cmax = 0, mine = 0;
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
     const K k = rk[i * ks];
     const uint64_t h = key_hash(k, identity);
@@ -162,7 +163,10 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
       uint32_t t = a.T[s];
       if (t == kEmpty32) {
         t = atomicCAS(&a.T[s], kEmpty32, i);
-        if (t == kEmpty32) break;
+        if (t == kEmpty32) {
+          ++mine;
+          break;
+        }
       }
       if (rk[t * ks] == k) {
         if (i < t) atomicMin(&a.T[s], i);   // T[s] only decreases: skip when already smaller
@@ -174,11 +178,14 @@ __device__ bool leaf_dedup(const K* rk, uint32_t m, uint32_t cap, bool identity,
   }
   cmin = __reduce_min_sync(0xFFFFFFFFu, cmin);
   cmax = __reduce_max_sync(0xFFFFFFFFu, cmax);
+  mine = __reduce_add_sync(0xFFFFFFFFu, mine);
   if (lane_id() == 0) {
     atomicMin(&s_cmin, cmin);
     atomicMax(&s_cmax, cmax);
+    atomicAdd(&s_groups, mine);
   }
   __syncthreads();
+  if (groups) *groups = s_groups;
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
     const uint32_t f = a.T[a.pos[i]];
     a.pos[i] = f;
@@ -194,8 +201,13 @@ __device__ void leaf_eq(const K* rk, const V* rv, K* ok, V* ov, uint32_t m, bool
                         LeafArrays a, uint32_t* red, bool hw = false) {
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
   const uint32_t cap = leaf_cap(m);
-  const bool one_cell = leaf_dedup(rk, m, cap, identity, a);
-  if (hw) {
+  uint32_t groups = 0;
+  const bool one_cell = leaf_dedup(rk, m, cap, identity, a, true, 1, &groups);
+  if (groups == m) {
+    // every key distinct (uniform keys): each record is its own group, so
+    // pass 1's (first index, index) order is the input order
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) a.pos[i] = i;
+  } else if (hw) {
     // Pass 1 with lane-ordered atomics (probe.cuh), walking only records of
     // groups with more than one record: a singleton group's record goes to
     // its group start directly (all-distinct leaves -- uniform keys --
@@ -281,9 +293,26 @@ k_leaf_eq_smem(const K* __restrict__ src_k, const V* __restrict__ src_v, K* __re
       }
       continue;
     }
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      rk[i] = src_k[(lf.lo + i) * ss];
-      if constexpr (kHasV) rv[i] = src_v[(lf.lo + i) * ss];
+    {   // all of the leaf's loads in flight at once (<= 4 records per thread)
+      constexpr int kPer = kLeafSmemMax / kLeafThreads;
+      K kr[kPer];
+      V vr[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t i = threadIdx.x + u * kLeafThreads;
+        if (i < m) {
+          kr[u] = src_k[(lf.lo + i) * ss];
+          if constexpr (kHasV) vr[u] = src_v[(lf.lo + i) * ss];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t i = threadIdx.x + u * kLeafThreads;
+        if (i < m) {
+          rk[i] = kr[u];
+          if constexpr (kHasV) rv[i] = vr[u];
+        }
+      }
     }
     __syncthreads();
     LeafArrays a = leaf_arrays(work, leaf_cap(m), m, false);
@@ -389,20 +418,23 @@ k_leaf_eq_global(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, 
 // mid leaves took 0.42 ms there.
 template <typename K, typename V>
 constexpr uint32_t kLeafMidMax = sizeof(K) + ValTraits<V>::bytes <= 16 ? 4096u : 2048u;
+// When every mid leaf of a launch has <= 2048 records (c5: all of them, c2's
+// too), the 2048-record shape holds two CTAs per SM (89 KB each for 16-byte
+// records instead of 179 KB).
+constexpr uint32_t kLeafMidSmall = 2048;
 
-template <typename K, typename V>
+template <typename K, typename V, uint32_t M = kLeafMidMax<K, V>>
 __host__ inline size_t leaf_mid_smem_bytes() {
-  constexpr uint32_t M = kLeafMidMax<K, V>;
   return static_cast<size_t>(M) * (sizeof(K) + ValTraits<V>::bytes) + leaf_words(M, false) * 4 + 64;
 }
 
-template <typename K, typename V>
+template <typename K, typename V, uint32_t M = kLeafMidMax<K, V>>
 __global__ void __launch_bounds__(kLeafThreads)
 k_leaf_eq_mid(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* __restrict__ A_v,
               const Leaf* __restrict__ leaves, uint32_t n_leaves, int in_a, int identity,
-              uint32_t* __restrict__ scratch, uint64_t words_per_cta, int hw, int s_pairs = 0) {
+              uint32_t* __restrict__ scratch, uint64_t words_per_cta, int hw, int s_pairs = 0,
+              uint64_t size_lo = 0, uint64_t size_hi = ~0ull) {   // leaves outside [size_lo, size_hi]: another launch
   constexpr bool kHasV = ValTraits<V>::bytes > 0;
-  constexpr uint32_t M = kLeafMidMax<K, V>;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t red[33];
   K* rk = reinterpret_cast<K*>(smem);
@@ -416,6 +448,7 @@ k_leaf_eq_mid(K* __restrict__ S_k, V* __restrict__ S_v, K* __restrict__ A_k, V* 
   const uint32_t ss = in_a ? 1u : (s_pairs ? 2u : 1u);
   for (uint32_t l = blockIdx.x; l < n_leaves; l += gridDim.x) {
     const Leaf lf = leaves[l];
+    if (lf.size < size_lo || lf.size > size_hi) continue;
     const uint32_t m = static_cast<uint32_t>(lf.size);
     if (m <= M) {
       if (m <= 1) {

@@ -184,16 +184,17 @@ inline void leaf_stats(const char* what, const Leaf* d_list, uint64_t count, cud
   std::vector<Leaf> h(count);
   SS_CUDA(cudaMemcpyAsync(h.data(), d_list, count * sizeof(Leaf), cudaMemcpyDeviceToHost, st));
   SS_CUDA(cudaStreamSynchronize(st));
-  uint64_t bins[12] = {}, recs = 0;
+  uint64_t bins[16] = {}, recs = 0;
   for (const Leaf& l : h) {
     int b = 0;
-    while (b < 11 && (1ull << b) < l.size) ++b;
+    while (b < 15 && (1ull << b) < l.size) ++b;
     ++bins[b];
     recs += l.size;
   }
   std::fprintf(stderr, "[leaf_stats] %s leaves=%llu records=%llu |", what, (unsigned long long)count,
                (unsigned long long)recs);
-  for (int b = 0; b < 12; ++b) std::fprintf(stderr, " <=%llu:%llu", 1ull << b, (unsigned long long)bins[b]);
+  for (int b = 0; b < 16; ++b)
+    if (bins[b]) std::fprintf(stderr, " <=%llu:%llu", 1ull << b, (unsigned long long)bins[b]);
   std::fprintf(stderr, "\n");
 }
 
@@ -356,7 +357,7 @@ struct SortEngine {
 
   // Global-scratch leaves; scr == nullptr uses the planned scratch.
   void run_leaves_global(Tracker& tr, const Leaf* d_list, uint64_t count, bool in_a, uint32_t* scr,
-                         uint64_t words) {
+                         uint64_t words, uint64_t max_size = ~0ull) {
     if (!count) return;
     leaf_stats("global", d_list, count, st);
     uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(count, leafg_grid));
@@ -366,11 +367,24 @@ struct SortEngine {
       k_leaf_lt<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count),
                                                     in_a, scr, words, aos ? 1 : 0);
     } else if (grid > 1) {   // planned mid leaves: shared-memory path up to kLeafMidMax
-      const size_t sm = leaf_mid_smem_bytes<K, V>();
-      auto kern = k_leaf_eq_mid<K, V>;
-      SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-      kern<<<grid, kLeafThreads, sm, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count), in_a, identity,
-                                           scr, words, hw_rank_ok() ? 1 : 0, aos ? 1 : 0);
+      auto launch = [&](auto kern, size_t sm, uint64_t lo, uint64_t hi) {
+        SS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        int per_sm = 0;
+        SS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLeafThreads, sm));
+        const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>(count, 148u * std::max(per_sm, 1)));
+        kern<<<std::min(g, grid), kLeafThreads, sm, st>>>(S_k, S_v, A_k, A_v, d_list, static_cast<uint32_t>(count),
+                                                         in_a, identity, scr, words, hw_rank_ok() ? 1 : 0,
+                                                         aos ? 1 : 0, lo, hi);
+      };
+      if constexpr (kLeafMidSmall < kLeafMidMax<K, V>) {
+        // leaves <= 2048 records at two CTAs per SM, the larger rest (c5: 5%)
+        // in a second launch of the one-CTA shape; each skips the other's
+        launch(k_leaf_eq_mid<K, V, kLeafMidSmall>, leaf_mid_smem_bytes<K, V, kLeafMidSmall>(), 0, kLeafMidSmall);
+        if (max_size > kLeafMidSmall)
+          launch(k_leaf_eq_mid<K, V>, leaf_mid_smem_bytes<K, V>(), kLeafMidSmall + 1, ~0ull);
+      } else {
+        launch(k_leaf_eq_mid<K, V>, leaf_mid_smem_bytes<K, V>(), 0, ~0ull);
+      }
     } else {
       k_leaf_eq_global<K, V><<<grid, kLeafThreads, 0, st>>>(S_k, S_v, A_k, A_v, d_list,
                                                             static_cast<uint32_t>(count), in_a, identity, scr, words,
@@ -543,7 +557,7 @@ struct SortEngine {
     SS_CUDA(cudaMemcpyAsync(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaMemcpyAsync(cur.data(), d_nodes, nn * sizeof(Node), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaStreamSynchronize(st));
-    const uint64_t n_w = misc[0], n_s = misc[1], n_g = misc[2], n_next = misc[3];
+    const uint64_t n_w = misc[0], n_s = misc[1], n_g = misc[2], n_next = misc[3], max_mid = misc[4];
     std::vector<Node> next(n_next);
     if (n_next) {
       SS_CUDA(cudaMemcpyAsync(next.data(), d_next, n_next * sizeof(Node), cudaMemcpyDeviceToHost, st));
@@ -569,7 +583,7 @@ struct SortEngine {
     tr.begin(kPhLeaves);
     run_leaves_warp(tr, d_leaf_w, n_w, leaves_in_a);
     run_leaves_smem(tr, d_leaf_s, n_s, leaves_in_a);
-    run_leaves_global(tr, d_leaf_g, n_g, leaves_in_a, nullptr, 0);
+    run_leaves_global(tr, d_leaf_g, n_g, leaves_in_a, nullptr, 0, max_mid);
 
     // forced leaves (stall valve / depth limit, core.py:459)
     std::vector<Node> keep;
