@@ -1,7 +1,7 @@
 """Benchmark: semisort Grecords/s on BASELINE.json's headline config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c5|c3|c4|graph] [--scaling weak|strong] [--mode eq|lt]
+                    [--workload c2|c5|c3|c4|c1|graph] [--scaling weak|strong] [--mode eq|lt]
 
 Workloads:
   c2 (default, the metric's config, BASELINE.json configs[1]): semisort of
@@ -12,6 +12,8 @@ Workloads:
      and Zipf(0.8) ranks over [1, 10^8] (minus 1), value = global index;
      weak (10^9 per GPU) or strong (8 x 10^9 in total) scaling.
   c3 / c4: collect_reduce(summing64) / histogram on one GPU (configs[2], [3]).
+  c1 (configs[0]): the reference's CPU-runnable 2^20 case; call latency,
+     the reference package timed on the same input, byte-compared.
   graph: CSR transpose.
 Inputs are synthetic, seeded and generated on the device (same families,
 parameters and sampler as the reference generator).
@@ -951,6 +953,96 @@ def graph_main(args):
     print(json.dumps(line), flush=True)
 
 
+def c1_main(args):
+    """--workload c1: BASELINE.json configs[0], the reference's CPU-runnable
+    case -- semisort of 2^20 (u64 key uniform in [0, 2^20), u64 value =
+    index), default TuningParams (seed 1).  Launch-bound on a GPU (~75 MB
+    of traffic; one host round trip per recursion level), so the line
+    reports the per-call latency next to the reference package timed on
+    the same input (all host cores), and whether the GPU output bytes equal
+    the reference's (`validated`)."""
+    import numpy as np
+    import torch
+
+    import paper_2304_10078_b200 as S
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    env = Env(0, 1, dev, False)
+    n = 1 << 20
+    rng = np.random.default_rng(1)
+    keys = rng.integers(0, n, n).astype(np.uint64)
+    vals = np.arange(n, dtype=np.uint64)
+    pristine = S.RecordArray(keys, vals)
+    work = pristine.copy()
+    params = S.TuningParams.for_input(n)
+    adp = S.UIntKeyAdapter()
+
+    def one(tel=None, times=None):
+        work.keys.copy_(pristine.keys)
+        work.values.copy_(pristine.values)
+        env.sync()
+        with env.timed(times if times is not None else []):
+            S.semisort(work, adp, "eq", params, telemetry=tel)
+
+    for _ in range(max(args.warmup, 3)):
+        one()
+    tel = S.Telemetry(timing=True)
+    times = []
+    steps = max(args.steps, 20)
+    with ClockSampler(0) as clk:
+        for _ in range(steps):
+            one(tel, times)
+    ms = statistics.median(times)
+    out_k, out_v = work.keys_host(), work.values_host()
+    # e2e: pinned host input -> public API -> host output, per call
+    hk, hv = torch.from_numpy(keys).pin_memory(), torch.from_numpy(vals).pin_memory()
+    ok_k, ok_v = torch.empty_like(hk).pin_memory(), torch.empty_like(hv).pin_memory()
+    e_times = []
+    for i in range(steps + 3):
+        env.sync()
+        t0 = time.perf_counter()
+        d = S.RecordArray(hk.to(dev, non_blocking=True), hv.to(dev, non_blocking=True))
+        S.semisort(d, adp, "eq", params)
+        ok_k.copy_(d.keys, non_blocking=True)
+        ok_v.copy_(d.values, non_blocking=True)
+        env.sync()
+        if i >= 3:
+            e_times.append((time.perf_counter() - t0) * 1e3)
+    e_ms = statistics.median(e_times)
+    cpu, validated = None, None
+    R = _reference_module()
+    if R is not None and not args.no_cpu:
+        workers = os.cpu_count() or 1
+        rt = []
+        for i in range(4):   # the reference protocol: 4 reps, median of the last 3 (cli.py:79-80)
+            data = R.RecordArray(keys.copy(), vals.copy())
+            t0 = time.perf_counter()
+            R.semisort(data, R.UIntKeyAdapter(), "eq", R.TuningParams.for_input(n, seed=1), workers=workers)
+            rt.append(time.perf_counter() - t0)
+        tc = statistics.median(rt[1:])
+        validated = bool(np.array_equal(np.asarray(data.keys), out_k) and np.array_equal(np.asarray(data.values),
+                                                                                         out_v))
+        cpu = {"value": n / tc / 1e9, "unit": "Grecords/s", "cores": workers, "kind": "reference",
+               "sample": f"the full c1 input: reference package semisort (baseline/_ref, workers={workers}), "
+                         f"median of the last 3 of 4 reps ({tc:.3f} s); host {_cpu_model()}"}
+    line = {"metric": "semisort Grecords/s (n=2^20 u64 k/v, uniform [0,2^20))", "value": n / (ms / 1e3) / 1e9,
+            "unit": "Grecords/s", "n_gpus": 1, "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (numpy default_rng(1), uniform keys, value = index)",
+            "config": {"workload": "c1: semisort n=2^20, uint64 key uniform [0, 2^20), value = index "
+                                   "(BASELINE.json configs[0]); median call latency",
+                       "params": "TuningParams.for_input(n) (seed 1)",
+                       "l2": "16 MB input, L2-resident: a launch-latency-bound config, not a roofline one"},
+            "phase_ms_per_step": {k: v / steps for k, v in tel.phase_ms.items()},
+            "gpu_launches": tel.kernel_launches // steps if tel.kernel_launches else None,
+            "clocks": clk.summary(),
+            "e2e": {"value": n / (e_ms / 1e3) / 1e9, "unit": "Grecords/s", "h2d_bytes_per_step": 16 * n,
+                    "d2h_bytes_per_step": 16 * n, "ms_per_step": e_ms},
+            "cpu_baseline": cpu, "validated": validated,
+            "validation": "GPU output bytes == the reference package's output bytes (same input, same params)"}
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------
 # launcher
 # ---------------------------------------------------------------------------
@@ -990,9 +1082,9 @@ def parse_args(argv=None):
     ap.add_argument("--validate", action="store_true", help="(default; kept for compatibility)")
     ap.add_argument("--mode", default="eq", choices=["eq", "lt"],
                     help="semisort mode: eq (default, the headline) or lt (semisort<, stable sort inside leaves)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5", "c3", "c4", "graph"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5", "c3", "c4", "c1", "graph"],
                     help="c2 (default, the headline semisort); c5 multi-GPU mix; c3 collect_reduce sum64; "
-                         "c4 histogram; graph: CSR transpose")
+                         "c4 histogram; c1 the 2^20 CPU-runnable case; graph: CSR transpose")
     return ap.parse_args(argv)
 
 
@@ -1004,9 +1096,9 @@ def main(argv=None):
         return 0
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(argv, args.gpus)
-    if args.workload in ("c3", "c4", "graph"):
+    if args.workload in ("c3", "c4", "c1", "graph"):
         if int(os.environ.get("RANK", "0")) == 0:
-            graph_main(args) if args.workload == "graph" else agg_main(args)
+            {"graph": graph_main, "c1": c1_main}.get(args.workload, agg_main)(args)
         return 0
     env = cuda_env()
     try:
