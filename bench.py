@@ -380,11 +380,14 @@ def _semisort_roofline(world, n_local, ms, tel, steps, peak_gbs, traffic):
              "frac_of_roofline": (n_local / t) / roof_rate})
 
 
-def _traffic():
-    """ncu DRAM bytes of the level-0 k_distribute1 launch (profiles/traffic.json)."""
+def _traffic(workload):
+    """Mean ncu DRAM bytes per k_distribute1 launch of one step of `workload`
+    (profiles/traffic.json, one `ncu --set full` capture), or None."""
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(tpath))
+        t = json.load(open(tpath))
+        ls = t[workload]["launches"]
+        return sum(x["dram_read"] + x["dram_write"] for x in ls) / len(ls), len(ls), t.get("note", "")
     except Exception:
         return None
 
@@ -452,12 +455,13 @@ def run_semisort(args, env: Env, hooks, emit=print):
     ms = env.max(ms_local)
     value = total / (ms / 1e3) / 1e9
     peak_gbs, peak_kind = measured_peaks()
-    tr = _traffic()
-    traffic = tr.get("k_distribute_bytes_per_launch") if (tr and w == "c2" and world == 1) else None
-    roof, step_roof = _semisort_roofline(world, n, ms, tel, args.steps, peak_gbs, traffic)
+    tr = _traffic(w) if (world == 1 and args.mode == "eq" and n == N_DEFAULT) else None
+    roof, step_roof = _semisort_roofline(world, n, ms, tel, args.steps, peak_gbs, tr[0] if tr else None)
     roof["peak_kind"] = peak_kind
-    if traffic is not None:
-        roof["traffic_note"] = tr.get("note", "ncu dram bytes of the level-0 launch")
+    if tr is not None:
+        launches = tr[1]
+        roof["alg_bytes_per_launch"] = tel.bucket_assignments / args.steps * 32 / launches
+        roof["traffic_note"] = f"mean over the step's {launches} distribute launches; " + tr[2]
 
     # validation of the last timed step's output (outside the timed region)
     valid, vdetail = None, None
@@ -870,7 +874,9 @@ def agg_main(args):
                        "l2": "256 MB buffer written before each step (flushes the 126 MB L2); input >= 4 GB"},
             "roofline": {"bound": "hbm", "kernel": "k_distribute1 (light-only scatter, all levels)",
                          "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                         "frac": (achieved / peak_gbs) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak_gbs) if achieved else None,
+                         "traffic": (_traffic(w) or (None,))[0] if n == N_DEFAULT else None,
+                         "alg_bytes_per_launch": moved * 2 * rec_b,
                          "peak_kind": peak_kind,
                          "bytes_model": f"{2 * rec_b} B per bucketed record (read + write {rec_b} B)"},
             "step_roofline": {"bytes_per_record": c["b_alg"], "achieved_gbs": c["b_alg"] * n / (ms / 1e3) / 1e9,
