@@ -245,9 +245,21 @@ k_fold_nodes(const K* __restrict__ src_k, const V* __restrict__ src_v, uint32_t 
     // fold is bound by shared-memory wavefronts, and at load <= 0.3 / small
     // key counts the overflow it avoids is rare)
     constexpr uint32_t W = Sh::kW;
-    const uint32_t b1 = home(k), b2 = (b1 + 1) & (NB - 1);
+    const uint32_t b1 = home(k);
     TK q1[W], q2[W];
     bucket_keys(tk, b1, q1);
+    {   // fast path: the key is already in its home bucket (~99% of c4's
+        // records; an out-of-line slow path with a 16-key unrolled stream
+        // loop was measured slower: 2.75 -> 4.33 ms)
+      uint32_t hit = 0;
+#pragma unroll
+      for (int i = 0; i < static_cast<int>(W); ++i) hit |= (q1[i] == k ? 1u : 0u) << i;
+      if (hit) {
+        c_red(cnt, W * b1 + (__ffs(hit) - 1));
+        return;
+      }
+    }
+    const uint32_t b2 = (b1 + 1) & (NB - 1);
     uint32_t slot = T, e1 = W, e2 = W;
 #pragma unroll
     for (int i = W - 1; i >= 0; --i) {
