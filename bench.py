@@ -444,8 +444,8 @@ def run_semisort(args, env: Env, hooks, emit=print):
         env.barrier()
         return out
 
-    for _ in range(args.warmup):
-        step()
+    for _ in range(args.warmup):   # same code path as the timed steps (phase events on)
+        step(hooks.telemetry())
     times = []
     tel = hooks.telemetry()
     with ClockSampler(env.device.index if env.cuda else None) as clk:
@@ -500,7 +500,8 @@ def run_semisort(args, env: Env, hooks, emit=print):
         line = {
             "metric": (WORKLOADS[w]["metric"] if args.mode == "eq" else "semisort< (lt) " + WORKLOADS[w]["metric"]),
             "value": value, "unit": "Grecords/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "ms_per_step": ms, "ms_steps_rank0": [round(t, 3) for t in times],
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (device-generated, seeded)",
             "config": {"workload": WORKLOADS[w]["desc"], "n_per_gpu": n, "n_total": total,
                        "params": "TuningParams.for_input(n) (reference defaults, seed 1)",
@@ -822,12 +823,16 @@ def agg_main(args):
             res = S.collect_reduce(src, adp, spec, params, telemetry=tel)
         return res
 
-    for _ in range(args.warmup):
-        one()
+    for _ in range(args.warmup):   # same code path as the timed steps (phase events on)
+        one(S.Telemetry(timing=True))
     tel = S.Telemetry(timing=True)
     times = []
     with ClockSampler(0) as clk:
+        res = None
         for _ in range(args.steps):
+            # drop the previous result first: while it is alive the caching allocator cannot reuse its
+            # blocks and the call pays a cudaMalloc inside the timed region (seen as 0.5-70 ms on step 2)
+            res = None
             res = one(tel, times)
     ms = sum(times) / len(times)
     groups = int(res.key_tensor.numel()) if res.key_tensor is not None else 0
@@ -866,7 +871,8 @@ def agg_main(args):
                "path": "RecordArray(pinned host tensors) -> collect_reduce -> (keys, aggs) to host"}
     cpu = None if args.no_cpu else agg_cpu_baseline(w, 1 << 22)
     line = {"metric": c["metric"], "value": value, "unit": "Grecords/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "ms_steps": [round(t, 3) for t in times],
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64" if c["key_bits"] == 64 else "u32",
             "data": "synthetic (device-generated, seeded)",
             "config": {"workload": c["desc"], "n_per_gpu": n, "groups": groups,
@@ -924,8 +930,8 @@ def graph_main(args):
             t = S.transpose(g, params, telemetry=tel)
         return t
 
-    for _ in range(args.warmup):
-        one()
+    for _ in range(args.warmup):   # same code path as the timed steps (phase events on)
+        one(S.Telemetry(timing=True))
     tel = S.Telemetry(timing=True)
     times = []
     with ClockSampler(0) as clk:
