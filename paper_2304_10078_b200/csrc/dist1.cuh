@@ -219,20 +219,31 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
       n_valid = static_cast<uint32_t>(total64);
       if (own) {
         uint32_t st[QP];   // packed tile starts of each owned pair (low | high << 16)
+        // the owned buckets' cursors as one vector per thread (scalar accesses
+        // at a stride of 2 QP words were 2 QP-way bank conflicts); entries at
+        // or past nb are padding of the 16-byte rounded rows
+        static_assert(QP == 2, "cursor rows are padded to 4 words: one uint4 (two pairs) per thread");
+        using CV = uint4;
+        constexpr int kCV = 1;
+        CV cur[kCV], wb[kCV];
+#pragma unroll
+        for (int c = 0; c < kCV; ++c) cur[c] = reinterpret_cast<const CV*>(cursor + 2 * j0)[c];
+        uint32_t* cw = reinterpret_cast<uint32_t*>(cur);
+        uint32_t* ww = reinterpret_cast<uint32_t*>(wb);
 #pragma unroll
         for (int q = 0; q < QP; ++q) {
-          const uint32_t b0 = 2 * (j0 + q);
           const uint32_t alo = a, ahi = a + lo[q];
           a = ahi + hi[q];
           st[q] = alo | (ahi << 16);
-          if (b0 < nb) {   // modular: cursor + (s - start) below
-            wbase[b0] = cursor[b0] - alo;
-            cursor[b0] += lo[q];
-          }
-          if (b0 + 1 < nb) {
-            wbase[b0 + 1] = cursor[b0 + 1] - ahi;
-            cursor[b0 + 1] += hi[q];
-          }
+          ww[2 * q] = cw[2 * q] - alo;   // modular: cursor + (s - start) below
+          cw[2 * q] += lo[q];
+          ww[2 * q + 1] = cw[2 * q + 1] - ahi;
+          cw[2 * q + 1] += hi[q];
+        }
+#pragma unroll
+        for (int c = 0; c < kCV; ++c) {
+          reinterpret_cast<CV*>(wbase + 2 * j0)[c] = wb[c];
+          reinterpret_cast<CV*>(cursor + 2 * j0)[c] = cur[c];
         }
 #pragma unroll
         for (int v = 0; v < NW; ++v) {   // tile position of warp v's first record per bucket
