@@ -293,6 +293,45 @@ __device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __re
         }
       }
     }
+    // L2 prefetch of the tile `pf` tiles ahead in this CTA's sequence (the
+    // current work item, then the one already claimed): the bulk copy into
+    // the stage then finds its lines in L2 instead of waiting behind the
+    // scattered stores (c2 distribute 12.64 -> 12.35 ms at pf = 2; 3 and 4
+    // tiles ahead were slower, 4-byte records did not gain).  SS_DIST_DEBUG
+    // bits 8-11 override pf (15 = off).
+    constexpr uint32_t kPfDefault = sizeof(K) + Cfg::kValBytes >= 16 ? 2u : 0u;
+    const uint32_t pf_dbg = (static_cast<uint32_t>(dbg) >> 8) & 15u;
+    if (const uint32_t pf = pf_dbg == 15u ? 0u : pf_dbg ? pf_dbg : kPfDefault) {
+      uint64_t fb = 0;
+      uint32_t fc = 0;
+      const uint64_t ahead = static_cast<uint64_t>(ptb) + static_cast<uint64_t>(pf) * T;
+      if (ahead < pw.len) {
+        fb = pw.begin + ahead;
+        fc = static_cast<uint32_t>(min(static_cast<uint64_t>(T), pw.len - ahead));
+      } else if (pnext < n_work) {
+        const uint64_t rem = (static_cast<uint64_t>(pw.len - ptb) + T - 1) / T;   // tiles left in the item, this one included
+        const uint64_t off = (pf - rem) * static_cast<uint64_t>(T);
+        if (pf >= rem && off < pwn.len) {
+          fb = pwn.begin + off;
+          fc = static_cast<uint32_t>(min(static_cast<uint64_t>(T), pwn.len - off));
+        }
+      }
+      if (fc) {
+        const Bulk16<uint16_t> fi(ids, n_src, fb, fc);
+        if (fi.ok) bulk_prefetch_l2(fi.src, fi.bytes);
+        if constexpr (SA) {
+          const Bulk16<Pair2<K>> fp(reinterpret_cast<const Pair2<K>*>(sk), n_src, fb, fc);
+          if (fp.ok) bulk_prefetch_l2(fp.src, fp.bytes);
+        } else {
+          const Bulk16<K> fk(sk, n_src, fb, fc);
+          if (fk.ok) bulk_prefetch_l2(fk.src, fk.bytes);
+          if constexpr (kHasV) {
+            const Bulk16<V> fv(sv, n_src, fb, fc);
+            if (fv.ok) bulk_prefetch_l2(fv.src, fv.bytes);
+          }
+        }
+      }
+    }
     ptb += T;
     if (ptb >= pw.len) {   // advance to the prefetched item, prefetch the next
       pwi = pnext;
