@@ -47,6 +47,20 @@ struct Dist1Cfg : DistCfg<K, V, TILE, NT, STAGES> {
   }
 };
 
+// Store with an L2 eviction policy (8- and 16-byte values; others plain).
+template <typename T>
+__device__ __forceinline__ void st_pol(T* p, const T& v, uint64_t pol) {
+  if constexpr (sizeof(T) == 16) {
+    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(&v);
+    asm volatile("st.global.L2::cache_hint.v2.b64 [%0], {%1, %2}, %3;" ::"l"(p), "l"(u.x), "l"(u.y), "l"(pol) : "memory");
+  } else if constexpr (sizeof(T) == 8) {
+    const unsigned long long u = *reinterpret_cast<const unsigned long long*>(&v);
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(u), "l"(pol) : "memory");
+  } else {
+    *p = v;
+  }
+}
+
 // SA: source in the pair scratch layout (keys at even, values at odd
 // K-words; sk points at the first key, sv is unused); DA: destination in
 // the pair layout -- a light record leaves as ONE 16-byte (8-byte for u32)
@@ -88,6 +102,13 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
   uint32_t* cntw = reinterpret_cast<uint32_t*>(p);   // [NW][pstride] u16 pairs
   for (uint32_t i = threadIdx.x; i < NW * pstride; i += blockDim.x) cntw[i] = 0;
   const int dbg = g_dist_debug;
+  // The scattered stores keep their lines in L2 (evict_last) until the
+  // work item's following tiles have completed them; the streamed input is
+  // evict_first (dist_producer).  Measured against plain stores: c3
+  // distribute 9.98 -> 9.50 ms, c2 12.62 -> 12.28; evict_first and
+  // evict_unchanged on the stores: no change.
+  uint64_t spol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(spol));
   const int w = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int b = 0; b < STAGES; ++b) {
@@ -347,12 +368,12 @@ k_distribute1(const K* __restrict__ sk, const V* __restrict__ sv, const uint16_t
         for (int k = 0; k < kB; ++k) {
           if constexpr (DA) {
             Pair2<K>* dP = reinterpret_cast<Pair2<K>*>(dk);
-            if (wk[k]) dP[dd[k]] = Pair2<K>{kk[k], static_cast<K>(vv[k])};
-            else if (ok[k]) reinterpret_cast<K*>(dk)[hbase + dd[k]] = static_cast<K>(vv[k]);
+            if (wk[k]) st_pol(dP + dd[k], Pair2<K>{kk[k], static_cast<K>(vv[k])}, spol);
+            else if (ok[k]) st_pol(reinterpret_cast<K*>(dk) + hbase + dd[k], static_cast<K>(vv[k]), spol);
           } else {
-            if (wk[k]) dk[dd[k]] = kk[k];
+            if (wk[k]) st_pol(dk + dd[k], kk[k], spol);
             if constexpr (kHasV) {
-              if (ok[k]) dv[dd[k]] = vv[k];
+              if (ok[k]) st_pol(dv + dd[k], vv[k], spol);
             }
           }
         }
