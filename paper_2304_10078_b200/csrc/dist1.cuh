@@ -56,6 +56,9 @@ __device__ __forceinline__ void st_pol(T* p, const T& v, uint64_t pol) {
   } else if constexpr (sizeof(T) == 8) {
     const unsigned long long u = *reinterpret_cast<const unsigned long long*>(&v);
     asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(u), "l"(pol) : "memory");
+  } else if constexpr (sizeof(T) == 4) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(&v);
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(u), "l"(pol) : "memory");
   } else {
     *p = v;
   }
