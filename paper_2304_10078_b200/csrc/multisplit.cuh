@@ -337,10 +337,10 @@ __device__ __forceinline__ void copy_span(T* __restrict__ dst, const T* __restri
     for (; i + 3 * nthreads < nv; i += 4 * nthreads) {   // 4 loads in flight per thread
       const uint4 x0 = __ldcs(s4 + i), x1 = __ldcs(s4 + i + nthreads), x2 = __ldcs(s4 + i + 2 * nthreads),
                   x3 = __ldcs(s4 + i + 3 * nthreads);
-      d4[i] = x0;
-      d4[i + nthreads] = x1;
-      d4[i + 2 * nthreads] = x2;
-      d4[i + 3 * nthreads] = x3;
+      __stcs(d4 + i, x0);
+      __stcs(d4 + i + nthreads, x1);
+      __stcs(d4 + i + 2 * nthreads, x2);
+      __stcs(d4 + i + 3 * nthreads, x3);
     }
     for (; i < nv; i += nthreads) d4[i] = s4[i];
     for (uint64_t i = v0 + nv * per + tid; i < hi; i += nthreads) dst[i] = src[i];
@@ -369,7 +369,7 @@ __device__ __forceinline__ void copy_span(T* __restrict__ dst, const T* __restri
 #pragma unroll
       for (int u = 0; u < 4; ++u) o[u] = pick(__ldcs(s4 + i + u * nthreads), __ldcs(s4 + i + u * nthreads + 1));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d4[i + u * nthreads] = o[u];
+      for (int u = 0; u < 4; ++u) __stcs(d4 + i + u * nthreads, o[u]);
     }
     for (; i < nv; i += nthreads) d4[i] = pick(__ldcs(s4 + i), __ldcs(s4 + i + 1));
     for (uint64_t k = head + nv * 4 + tid; k < words; k += nthreads) dw[k] = sw[k];
@@ -415,7 +415,7 @@ __device__ __forceinline__ void fill_span(K* __restrict__ dst, uint64_t lo, uint
 #pragma unroll
   for (uint64_t q = 0; q < per; ++q) pk[q] = key;
   uint4* d4 = reinterpret_cast<uint4*>(dst + v0);
-  for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) d4[i] = pat;
+  for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) __stcs(d4 + i, pat);
   for (uint64_t i = v0 + nv * per + threadIdx.x; i < hi; i += blockDim.x) dst[i] = key;
 }
 
