@@ -136,10 +136,15 @@ inline void launch_distribute(const K* sk, const V* sv, const uint16_t* ids, K* 
       }
       launch_distribute1_t<K, V, TILE, false, false>(SS_DIST_ARGS, key_below, cstride);
     };
+    bool done = false;
     if constexpr (kDist8k<K, V>) {
-      if (t1 == 8192) return go.template operator()<8192>();
+      if (t1 == 8192) {
+        go.template operator()<8192>();
+        done = true;
+      }
     }
-    if (t1 == 4096) go.template operator()<4096>();
+    if (done) {
+    } else if (t1 == 4096) go.template operator()<4096>();
     else go.template operator()<2048>();
   } else {
     if (src_pairs || dst_pairs) throw Fail(SS_ERR_RESOURCE, "pair scratch layout needs the single-pass distribute");
