@@ -297,9 +297,10 @@ __device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __re
     // current work item, then the one already claimed): the bulk copy into
     // the stage then finds its lines in L2 instead of waiting behind the
     // scattered stores (c2 distribute 12.64 -> 12.35 ms at pf = 2; 3 and 4
-    // tiles ahead were slower, 4-byte records did not gain).  SS_DIST_DEBUG
-    // bits 8-11 override pf (15 = off).
-    constexpr uint32_t kPfDefault = sizeof(K) + Cfg::kValBytes >= 16 ? 2u : 0u;
+    // tiles ahead were slower, 4-byte records did not gain; with evict_last
+    // stores and an evict_last hint on the prefetch, one tile ahead is best:
+    // 12.11 -> 11.96 ms).  SS_DIST_DEBUG bits 8-11 override pf (15 = off).
+    constexpr uint32_t kPfDefault = sizeof(K) + Cfg::kValBytes >= 16 ? 1u : 0u;
     const uint32_t pf_dbg = (static_cast<uint32_t>(dbg) >> 8) & 15u;
     if (const uint32_t pf = pf_dbg == 15u ? 0u : pf_dbg ? pf_dbg : kPfDefault) {
       uint64_t fb = 0;
@@ -317,6 +318,9 @@ __device__ __forceinline__ void dist_producer(unsigned char* smem, const K* __re
         }
       }
       if (fc) {
+        // prefetched lines are evict_last until the stage copy (evict_first) takes them
+        const uint64_t ppol = l2_evict_last_policy();
+        auto bulk_prefetch_l2 = [&](const void* src, uint32_t bytes) { ss::bulk_prefetch_l2_hint(src, bytes, ppol); };
         const Bulk16<uint16_t> fi(ids, n_src, fb, fc);
         if (fi.ok) bulk_prefetch_l2(fi.src, fi.bytes);
         if constexpr (SA) {
